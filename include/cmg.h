@@ -1,0 +1,129 @@
+/*
+ * cmg.h -- C ABI of the B200 multigrid curvature-energy solver (libcmg.so).
+ *
+ * Drop-in boundary for the reference package `curvemg` (arXiv 2204.07921).
+ * The reference has no FFI: its boundary is the Python call
+ *     curvemg.denoise(f: Image, config: SolverConfig, reference=None)
+ *         -> (Image, ConvergenceTrace)
+ * (/root/reference/pkg/src/curvemg/driver.py:261-314, re-exported at
+ * __init__.py:3-10).  Each entry point below names the reference function it
+ * replaces; the Python shim paper_2204_07921_b200.driver binds them through
+ * ctypes and keeps the reference's names, argument meaning and exceptions.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; images are row-major, batch x m x n,
+ *    element type double (CMG_F64) or float (CMG_F32) as chosen at plan time;
+ *  - every function returns a status code; cmg_last_error() gives the
+ *    message of the last failure on the calling thread;
+ *  - the caller owns host buffers, the plan owns device buffers, its CUDA
+ *    stream and its CUDA graphs.  One plan per host thread; calls are
+ *    synchronous with respect to the caller.
+ */
+#ifndef CMG_H
+#define CMG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define CMG_OK 0
+#define CMG_EINVAL 1        /* ValueError: SolverConfig / Image validation (driver.py:56-72, image.py:51-58) */
+#define CMG_NOT_CONVERGED 2 /* ran max_outer cycles without meeting epsilon (trace.converged == False) */
+#define CMG_DIVERGED 3      /* SolverDivergence: non-finite energy (driver.py:302-303) */
+#define CMG_ECUDA 4         /* CUDA runtime failure */
+#define CMG_ENONFINITE 5    /* ValueError("corrections must be finite") (hierarchy.py:122-123) */
+
+/* plan options */
+#define CMG_MODE_MEAN 0  /* SolverConfig.mode == "mean"     (driver.py:47) */
+#define CMG_MODE_GAUSS 1 /* SolverConfig.mode == "gaussian" */
+#define CMG_F64 0
+#define CMG_F32 1
+#define CMG_PREC_EXACT 0 /* NumPy operation order, bit-identical to the reference in fp64 */
+#define CMG_PREC_FAST 1  /* closed-form pair distances + rsqrt (mean mode only) */
+#define CMG_STOP_REL_ENERGY 0
+#define CMG_STOP_REL_U 1
+
+typedef struct cmg_plan cmg_plan;
+
+/* library version (major*10000 + minor*100 + patch) */
+int cmg_version(void);
+
+/* message of the last error on this thread ("" if none) */
+const char* cmg_last_error(void);
+
+/* number of visible CUDA devices */
+int cmg_device_count(int* count);
+
+/*
+ * Create a solver plan for `batch` images of m x n pixels with `layers`
+ * levels (hierarchy.build_hierarchy, hierarchy.py:83-91: 1 <= layers <= 6).
+ * Replaces the per-call setup at the top of driver.denoise (driver.py:267-276).
+ */
+int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mode, int dtype, int precision,
+                    int device);
+int cmg_plan_destroy(cmg_plan* plan);
+
+/*
+ * Solve from HOST buffers (driver.denoise, driver.py:261-314).
+ *   f_host        batch*m*n input images (element type of the plan)
+ *   ref_host      optional clean images for the per-cycle PSNR (NULL: no PSNR)
+ *   u_host_out    batch*m*n restored images
+ *   alpha..peak   SolverConfig fields (driver.py:45-53) and Image.peak
+ *   energy, rel_energy, rel_u, psnr, seconds
+ *                 optional (NULL) trace outputs, batch x (max_outer+1)
+ *                 doubles each (TraceRecord fields, driver.py:83-91)
+ *   iterations    batch ints: ConvergenceTrace.iterations
+ *   status        batch ints: CMG_OK (converged), CMG_NOT_CONVERGED,
+ *                 CMG_DIVERGED or CMG_ENONFINITE per image
+ * Returns CMG_OK if every image converged, otherwise the first non-OK
+ * per-image status (or CMG_EINVAL / CMG_ECUDA).
+ */
+int cmg_solve(cmg_plan* plan, const void* f_host, const void* ref_host, void* u_host_out, double alpha,
+              double epsilon, int max_outer, int inner_iters, int stop_rule, int full_vcycle, double peak,
+              double* energy, double* rel_energy, double* rel_u, double* psnr, double* seconds, int* iterations,
+              int* status);
+
+/*
+ * Same as cmg_solve with DEVICE pointers (inputs already resident in HBM).
+ * Trace outputs are still host pointers.
+ */
+int cmg_solve_device(cmg_plan* plan, const void* f_dev, const void* ref_dev, void* u_dev_out, double alpha,
+                     double epsilon, int max_outer, int inner_iters, int stop_rule, int full_vcycle, double peak,
+                     double* energy, double* rel_energy, double* rel_u, double* psnr, double* seconds,
+                     int* iterations, int* status);
+
+/*
+ * One level visit -- the four colour sweeps of driver.sweep_layer
+ * (driver.py:225-251) -- on host buffers: u_host (batch*m*n) is updated in
+ * place, f_host is the noisy input.  Parity-test entry point.
+ */
+int cmg_sweep_layer(cmg_plan* plan, void* u_host, const void* f_host, int layer, double alpha, int inner_iters);
+
+/* tangent.energy (tangent.py:328-341) for each image: energy_out[batch] */
+int cmg_energy(cmg_plan* plan, const void* u_host, const void* f_host, double alpha, double* energy_out);
+
+/* tangent.plane_set (tangent.py:95-133) as compiled into the kernels:
+ * writes count*6 ints (x0,x1,y0,y1,z0,z1) and count ds2 values; returns count. */
+int cmg_plane_table(int layer, int* offsets, double* ds2);
+
+/* Launch statistics of the last solve: number of kernels launched (all
+ * nodes executed, including early-exit ones) and cycles executed. */
+int cmg_plan_stats(cmg_plan* plan, long long* kernel_launches, int* cycles_run, double* device_ms);
+
+/*
+ * Time one sweep kernel with CUDA events on the plan's stream:
+ * `reps` launches of the level-`layer` colour-`color` kernel (color < 0: all
+ * four colours of the level) on the data left by the last solve.  Writes the
+ * mean duration per launch in milliseconds.  Used by bench.py's roofline.
+ */
+int cmg_time_sweep(cmg_plan* plan, int layer, int color, int reps, double* ms_per_launch);
+
+/* Pinned host memory helpers (for host<->device copies at full PCIe rate). */
+void* cmg_host_alloc(unsigned long long bytes);
+int cmg_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CMG_H */

@@ -1,0 +1,99 @@
+"""Pin the CPU oracle (oracle/cmg_oracle.c) against fixtures produced by the
+REFERENCE implementation itself (tests/golden/make_golden.py).
+
+Bar: bit-exact (IEEE binary64) for padding, sweeps, energies, denoise
+outputs and traces.
+"""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2204_07921_b200 import planes as P
+from paper_2204_07921_b200 import synth
+
+
+@pytest.fixture(scope="module")
+def sweeps(golden_dir):
+    meta = json.loads((golden_dir / "sweeps.json").read_text())
+    arr = np.load(golden_dir / "sweeps.npz")
+    return meta, arr
+
+
+def test_plane_tables_match_reference(golden_dir):
+    g = json.loads((golden_dir / "planes.json").read_text())
+    for j in range(1, 7):
+        ref = np.array(g[str(j)])
+        offs, ds2 = O.plane_table(j)
+        assert np.array_equal(offs, ref[:, :6].astype(int)), j
+        assert np.array_equal(ds2, ref[:, 6]), j
+        mine = P.planes(j)
+        assert [[*p.x, *p.y, *p.z, p.ds2] for p in mine] == g[str(j)]
+
+
+def test_pad_matches_numpy_reference(sweeps):
+    meta, arr = sweeps
+    for ci, (shape, widths) in enumerate(meta["pads"]):
+        a = arr[f"pad{ci}_in"]
+        out = O.pad_odd(a, widths)
+        assert np.array_equal(out, arr[f"pad{ci}_out"]), (shape, widths)
+
+
+def test_sweep_layer_bitexact(sweeps):
+    meta, arr = sweeps
+    assert len(meta["sweeps"]) > 100
+    for c in meta["sweeps"]:
+        k = c["key"]
+        out = O.sweep_layer(arr[f"{k}_u"], arr[f"{k}_f"], c["layer"], c["mode"], c["inner_iters"], c["alpha"])
+        assert np.array_equal(out, arr[f"{k}_out"]), c
+
+
+def test_energy_bitexact(sweeps):
+    meta, arr = sweeps
+    for c in meta["energies"]:
+        k = c["key"]
+        e = O.energy(arr[f"{k}_u"], arr[f"{k}_f"], 0.06, c["mode"])
+        assert e == c["energy"], c
+
+
+def test_denoise_small_bitexact(golden_dir):
+    meta = json.loads((golden_dir / "denoise_small.json").read_text())
+    arr = np.load(golden_dir / "denoise_small.npz")
+    for c in meta:
+        k = c["key"]
+        r = O.denoise(arr[f"{k}_f"], alpha=0.06, mode=c["mode"], layers=c["layers"], epsilon=c["epsilon_used"],
+                      max_outer=c["max_outer"], inner_iters=c["inner_iters"], stop_rule=c["stop_rule"],
+                      full_vcycle=c["full_vcycle"], reference=arr[f"{k}_clean"], peak=1.0)
+        assert r["iterations"] == c["iterations"], k
+        assert r["converged"] == c["converged"], k
+        assert np.array_equal(r["u"], arr[f"{k}_u"]), k
+        assert np.array_equal(r["energies"], np.array(c["energies"])), k
+        assert np.array_equal(r["psnr"], np.array(c["psnr"])), k
+        assert np.array_equal(r["rel_u"][1:], np.array(c["rel_u"][1:])), k
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", ["c1_J6", "c1_J3", "c4_img0", "c2_J3"])
+def test_baseline_config_trajectories(golden_dir, name):
+    g = json.loads((golden_dir / "configs.json").read_text())[name]
+    f, cl = synth.config_input(g["config"], 0, fp32=g["fp32_input"])
+    assert _sha(f) == g["f_sha256"]
+    r = O.denoise(f, alpha=0.06, mode=g["mode"], layers=g["layers"], epsilon=g["epsilon"],
+                  max_outer=g["max_outer"], reference=cl, peak=1.0, threads=O.max_threads())
+    assert r["iterations"] == g["iterations"]
+    assert np.array_equal(r["energies"], np.array(g["energies"]))
+    assert np.array_equal(r["psnr"], np.array(g["psnr"]))
+    assert _sha(r["u"]) == g["u_sha256"]
+
+
+def test_numpy_pairwise_restatement():
+    rng = np.random.default_rng(0)
+    for n in (1, 7, 8, 9, 127, 128, 129, 1000, 4096 + 3, 65536):
+        a = rng.standard_normal(n) * np.exp(rng.standard_normal(n) * 4)
+        assert O.lib().orc_pairwise_sum(a.ctypes.data_as(O._dp), n) == a.sum()
