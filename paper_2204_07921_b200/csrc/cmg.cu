@@ -24,7 +24,7 @@
 #include <vector>
 
 #include "../../include/cmg.h"
-#include "cmg_kernels.cuh"
+#include "cmg_plan.h"
 
 using namespace cmg;
 
@@ -43,190 +43,15 @@ int fail(int code, const std::string& msg) {
         if (e_ != cudaSuccess) return fail(CMG_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-struct Level {
-    int layer = 0, s = 0, r = 0, mj = 0, nj = 0, mp = 0, np = 0;
-    bool general = false;  // needs numpy's iterated/singleton reflection -> padded snapshot
-    int H = 0, W = 0;
-    long long pstride = 0;
-    void* fpad = nullptr;
-};
-
 inline bool single_chunk(int len, int pad_after) { return len >= 2 && pad_after <= len - 1; }
 
 }  // namespace
 
-struct cmg_plan {
-    int m = 0, n = 0, B = 0, layers = 0, mode = 0, dtype = 0, prec = 0, device = 0;
-    size_t esz = 8;
-    long long N = 0;
-    cudaStream_t stream = nullptr;
-    void *u = nullptr, *uprev = nullptr, *f = nullptr, *ref = nullptr, *upad = nullptr, *epad = nullptr;
-    size_t upad_elems = 0;
-    bool egeneral = false;
-    int eH = 0, eW = 0;
-    long long epstride = 0;
-    Level lv[7];
-    double* partials = nullptr;
-    int nbx = 1;
-    ImgState* st = nullptr;
-    int* ndone = nullptr;
-    int* iters = nullptr;
-    double* eonly = nullptr;
-    SolveParams* P = nullptr;
-    double* tr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    int cap = 0;
-    // graphs
-    cudaGraphExec_t exec = nullptr;
-    int gkey = -1;
-    bool use_while = true;
-    int nodes_per_cycle = 0;
-    // stats
-    long long launches = 0;
-    int cycles_run = 0;
-    float dev_ms = 0.f;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    // launch counter during enqueue
-    int enq = 0;
-};
-
 namespace {
-
-// ---------------------------------------------------------------------------
-// enqueue helpers (used directly and under stream capture)
-// ---------------------------------------------------------------------------
-template <typename T>
-void enqueue_pad(cmg_plan* P, const void* src, void* dst, int H, int W, long long pstride, int bot, int rgt,
-                 bool gate) {
-    const ImgState* st = gate ? P->st : nullptr;
-    int blocks = (int)std::min<long long>((P->N + 255) / 256, 4096);
-    k_pad_copy<T><<<dim3(blocks, P->B), 256, 0, P->stream>>>((const T*)src, P->N, (T*)dst, pstride, P->m, P->n, W,
-                                                             st);
-    k_pad_axis<T><<<dim3((P->n + 127) / 128, P->B), 128, 0, P->stream>>>((T*)dst, pstride, 0, P->m, P->n, H, W,
-                                                                         bot, rgt, st);
-    k_pad_axis<T><<<dim3((H + 127) / 128, P->B), 128, 0, P->stream>>>((T*)dst, pstride, 1, P->m, P->n, H, W, bot,
-                                                                      rgt, st);
-    P->enq += 3;
-}
-
-template <typename T, int LAYER, int MODE, int PREC>
-void launch_tpp(const SweepArgs<T>& a, bool padded, int B, cudaStream_t s) {
-    dim3 blk(32, 8);
-    dim3 grd((a.wc + 31) / 32, (a.hc + 7) / 8, B);
-    if (padded)
-        k_sweep_tpp<T, LAYER, MODE, PREC, SRC_PADDED><<<grd, blk, 0, s>>>(a);
-    else
-        k_sweep_tpp<T, LAYER, MODE, PREC, SRC_INPLACE><<<grd, blk, 0, s>>>(a);
-}
-
-template <typename T, int MODE, int PREC>
-void dispatch_tpp_layer(const SweepArgs<T>& a, bool padded, int B, cudaStream_t s) {
-    switch (a.layer) {
-        case 1: launch_tpp<T, 1, MODE, PREC>(a, padded, B, s); break;
-        case 2: launch_tpp<T, 2, MODE, PREC>(a, padded, B, s); break;
-        default: launch_tpp<T, 3, MODE, PREC>(a, padded, B, s); break;
-    }
-}
-
-template <typename T>
-void enqueue_sweep(cmg_plan* P, int layer, int color) {
-    Level& L = P->lv[layer];
-    const int p = color >> 1, q = color & 1;
-    const int hc = (L.mj - p + 1) / 2, wc = (L.nj - q + 1) / 2;
-    if (hc <= 0 || wc <= 0) return;
-    if (L.general) enqueue_pad<T>(P, P->u, P->upad, L.H, L.W, L.pstride, 1 + L.mp - P->m, 1 + L.np - P->n, true);
-    SweepArgs<T> a;
-    a.u = (T*)P->u;
-    a.f = (const T*)P->f;
-    a.istride = P->N;
-    a.upad = (const T*)P->upad;
-    a.fpad = (const T*)L.fpad;
-    a.pstride = L.pstride;
-    a.W = L.W;
-    a.m = P->m;
-    a.n = P->n;
-    a.layer = layer;
-    a.s = L.s;
-    a.r = L.r;
-    a.p = p;
-    a.q = q;
-    a.hc = hc;
-    a.wc = wc;
-    a.flat = (wc == 1);
-    a.single = (hc * wc == 1);
-    a.P = P->P;
-    a.st = P->st;
-    const bool padded = L.general;
-    if (layer <= 3) {
-        if (P->mode == CMG_MODE_GAUSS)
-            dispatch_tpp_layer<T, MODE_GAUSS, PREC_EXACT>(a, padded, P->B, P->stream);
-        else if (P->prec == CMG_PREC_FAST)
-            dispatch_tpp_layer<T, MODE_MEAN, PREC_FAST>(a, padded, P->B, P->stream);
-        else
-            dispatch_tpp_layer<T, MODE_MEAN, PREC_EXACT>(a, padded, P->B, P->stream);
-    } else {
-        dim3 grd(wc, hc, P->B);
-        if (P->mode == CMG_MODE_GAUSS) {
-            if (padded)
-                k_sweep_bpp<T, MODE_GAUSS, SRC_PADDED><<<grd, 128, 0, P->stream>>>(a);
-            else
-                k_sweep_bpp<T, MODE_GAUSS, SRC_INPLACE><<<grd, 128, 0, P->stream>>>(a);
-        } else {
-            if (padded)
-                k_sweep_bpp<T, MODE_MEAN, SRC_PADDED><<<grd, 128, 0, P->stream>>>(a);
-            else
-                k_sweep_bpp<T, MODE_MEAN, SRC_INPLACE><<<grd, 128, 0, P->stream>>>(a);
-        }
-    }
-    P->enq += 1;
-}
-
-template <typename T>
-__global__ void k_copy(const T* __restrict__ src, T* __restrict__ dst, long long N, const ImgState* st) {
-    const int b = blockIdx.y;
-    if (st[b].done) return;
-    const long long off = (long long)b * N;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (long long)gridDim.x * blockDim.x)
-        dst[off + e] = src[off + e];
-}
 
 __global__ void k_cond(cudaGraphConditionalHandle h, const int* ndone, int B, int* iters) {
     *iters += 1;
     cudaGraphSetConditional(h, (*ndone < B) ? 1u : 0u);
-}
-
-template <typename T>
-void enqueue_energy(cmg_plan* P, bool has_ref, double* eonly, int initial) {
-    if (P->egeneral) enqueue_pad<T>(P, P->u, P->epad, P->eH, P->eW, P->epstride, 1, 1, !initial && !eonly);
-    EnergyArgs ea;
-    ea.u = P->u;
-    ea.f = P->f;
-    ea.uprev = P->uprev;
-    ea.ref = has_ref ? P->ref : nullptr;
-    ea.upad = P->epad;
-    ea.istride = P->N;
-    ea.pstride = P->epstride;
-    ea.m = P->m;
-    ea.n = P->n;
-    ea.W = P->eW;
-    ea.mode = P->mode;
-    ea.nbx = P->nbx;
-    ea.partials = P->partials;
-    ea.st = P->st;
-    if (P->egeneral)
-        k_energy<T, SRC_PADDED><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea);
-    else
-        k_energy<T, SRC_INPLACE><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea);
-    TraceArgs ta;
-    ta.energy = P->tr[0];
-    ta.rel_e = P->tr[1];
-    ta.rel_u = P->tr[2];
-    ta.psnr = P->tr[3];
-    ta.seconds = P->tr[4];
-    ta.cap = P->cap;
-    ta.ndone = P->ndone;
-    ta.eonly = eonly;
-    k_finalize<<<P->B, 256, 0, P->stream>>>(P->partials, P->nbx, P->P, P->st, ta, initial);
-    P->enq += 2;
 }
 
 std::vector<int> layer_sequence(int layers, int full) {
@@ -239,16 +64,20 @@ std::vector<int> layer_sequence(int layers, int full) {
 
 template <typename T>
 void enqueue_cycle_T(cmg_plan* P, int full, bool has_ref) {
-    const long long N = P->N;
-    int blocks = (int)std::min<long long>((N + 255) / 256, 2048);
-    k_copy<T><<<dim3(blocks, P->B), 256, 0, P->stream>>>((const T*)P->u, (T*)P->uprev, N, P->st);
-    P->enq += 1;
+    enqueue_copy_prev<T>(P);
     for (int j : layer_sequence(P->layers, full))
         for (int c = 0; c < 4; ++c) enqueue_sweep<T>(P, j, c);
     enqueue_energy<T>(P, has_ref, nullptr, 0);
 }
 
 void enqueue_cycle(cmg_plan* P, int full, bool has_ref) {
+    if (P->fused) {
+        if (P->dtype == CMG_F64)
+            enqueue_body_fused<double>(P, full, has_ref);
+        else
+            enqueue_body_fused<float>(P, full, has_ref);
+        return;
+    }
     if (P->dtype == CMG_F64)
         enqueue_cycle_T<double>(P, full, has_ref);
     else
@@ -357,14 +186,6 @@ void fill_params(cmg_plan* P, SolveParams& sp, double alpha, double eps, int max
     }
 }
 
-template <typename T>
-void enqueue_fpads(cmg_plan* P) {
-    for (int j = 1; j <= P->layers; ++j) {
-        Level& L = P->lv[j];
-        if (L.general) enqueue_pad<T>(P, P->f, L.fpad, L.H, L.W, L.pstride, 1 + L.mp - P->m, 1 + L.np - P->n, false);
-    }
-}
-
 int set_device(cmg_plan* P) {
     CK(cudaSetDevice(P->device));
     return CMG_OK;
@@ -383,49 +204,67 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
     CK(cudaMemcpyAsync(P->P, &sp, sizeof(sp), cudaMemcpyHostToDevice, P->stream));
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
     CK(cudaMemsetAsync(P->ndone, 0, sizeof(int) * 2, P->stream));
-    rc = build_graph(P, full, has_ref);
-    if (rc) return rc;
-    CK(cudaEventRecord(P->e0, P->stream));
-    P->enq = 0;
-    const size_t bytes = P->esz * (size_t)P->N * P->B;
-    CK(cudaMemcpyAsync(P->u, P->f, bytes, cudaMemcpyDeviceToDevice, P->stream));
-    CK(cudaMemcpyAsync(P->uprev, P->f, bytes, cudaMemcpyDeviceToDevice, P->stream));
-    if (P->dtype == CMG_F64) {
-        enqueue_fpads<double>(P);
-        enqueue_energy<double>(P, has_ref, nullptr, 1);
-    } else {
-        enqueue_fpads<float>(P);
-        enqueue_energy<float>(P, has_ref, nullptr, 1);
-    }
-    CK(cudaGetLastError());
-    const int init_launches = P->enq;
     int cycles = 0;
-    if (P->use_while) {
-        CK(cudaGraphLaunch(P->exec, P->stream));
+    if (P->persist) {
+        CK(cudaEventRecord(P->e0, P->stream));
+        P->enq = 0;
+        cudaError_t e = (P->dtype == CMG_F64) ? persist_launch<double>(P, has_ref, full)
+                                              : persist_launch<float>(P, has_ref, full);
+        if (e != cudaSuccess) return fail(CMG_ECUDA, std::string("persistent launch: ") + cudaGetErrorString(e));
         CK(cudaEventRecord(P->e1, P->stream));
         CK(cudaStreamSynchronize(P->stream));
-        CK(cudaMemcpy(&cycles, P->iters, sizeof(int), cudaMemcpyDeviceToHost));
+        P->launches = P->enq;
     } else {
-        int chunk = 1, launched = 0;
-        while (true) {
-            const int c = std::min(chunk, max_outer - launched);
-            for (int i = 0; i < c; ++i) CK(cudaGraphLaunch(P->exec, P->stream));
-            launched += c;
-            int nd = 0;
-            CK(cudaMemcpyAsync(&nd, P->ndone, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
-            CK(cudaStreamSynchronize(P->stream));
-            if (nd >= P->B || launched >= max_outer) break;
-            chunk = std::min(chunk * 2, 16);
+        rc = build_graph(P, full, has_ref);
+        if (rc) return rc;
+        CK(cudaEventRecord(P->e0, P->stream));
+        P->enq = 0;
+        const size_t bytes = P->esz * (size_t)P->N * P->B;
+        CK(cudaMemcpyAsync(P->u, P->f, bytes, cudaMemcpyDeviceToDevice, P->stream));
+        if (!P->fused) CK(cudaMemcpyAsync(P->uprev, P->f, bytes, cudaMemcpyDeviceToDevice, P->stream));
+        if (P->dtype == CMG_F64) {
+            enqueue_fpads<double>(P);
+            enqueue_energy_ptrs<double>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1);
+        } else {
+            enqueue_fpads<float>(P);
+            enqueue_energy_ptrs<float>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1);
         }
-        CK(cudaEventRecord(P->e1, P->stream));
-        CK(cudaStreamSynchronize(P->stream));
-        cycles = launched;
+        CK(cudaGetLastError());
+        const int init_launches = P->enq;
+        if (P->use_while) {
+            CK(cudaGraphLaunch(P->exec, P->stream));
+            CK(cudaEventRecord(P->e1, P->stream));
+            CK(cudaStreamSynchronize(P->stream));
+            CK(cudaMemcpy(&cycles, P->iters, sizeof(int), cudaMemcpyDeviceToHost));
+        } else {
+            int chunk = 1, launched = 0;
+            const int per = P->fused ? 2 : 1;
+            const int maxb = (max_outer + per - 1) / per;
+            while (true) {
+                const int c = std::min(chunk, maxb - launched);
+                for (int i = 0; i < c; ++i) CK(cudaGraphLaunch(P->exec, P->stream));
+                launched += c;
+                int nd = 0;
+                CK(cudaMemcpyAsync(&nd, P->ndone, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
+                CK(cudaStreamSynchronize(P->stream));
+                if (nd >= P->B || launched >= maxb) break;
+                chunk = std::min(chunk * 2, 16);
+            }
+            CK(cudaEventRecord(P->e1, P->stream));
+            CK(cudaStreamSynchronize(P->stream));
+            cycles = launched;
+        }
+        P->launches = (long long)init_launches + (long long)cycles * P->nodes_per_cycle;
     }
     CK(cudaEventElapsedTime(&P->dev_ms, P->e0, P->e1));
-    P->cycles_run = cycles;
-    P->launches = (long long)init_launches + (long long)cycles * P->nodes_per_cycle;
     std::vector<ImgState> hs(P->B);
     CK(cudaMemcpy(hs.data(), P->st, sizeof(ImgState) * P->B, cudaMemcpyDeviceToHost));
+    if (P->persist || P->fused) {
+        cycles = 0;
+        for (int b = 0; b < P->B; ++b)
+            cycles = std::max(cycles, hs[b].cycle + ((hs[b].status == ST_DIVERGED || hs[b].status == ST_NONFINITE) ? 1 : 0));
+    }
+    P->cycles_run = cycles;
     double* outs[5] = {energy, rel_e, rel_u, psnr, seconds};
     for (int i = 0; i < 5; ++i) {
         if (!outs[i]) continue;
@@ -478,7 +317,7 @@ int cmg_plan_destroy(cmg_plan* P) {
     cudaSetDevice(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     if (P->exec) cudaGraphExecDestroy(P->exec);
-    void* ptrs[] = {P->u, P->uprev, P->f, P->ref, P->upad, P->epad, P->partials, P->st, P->ndone, P->eonly, P->P};
+    void* ptrs[] = {P->u, P->uprev, P->ubuf[2], P->f, P->ref, P->upad, P->epad, P->partials, P->st, P->ndone, P->eonly, P->P};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 5; ++i)
@@ -517,6 +356,10 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     P->N = (long long)m * n;
     const char* nw = getenv("CMG_NO_WHILE");
     P->use_while = !(nw && nw[0] == '1');
+    if (const char* t2 = getenv("CMG_TS2")) P->ts2 = atoi(t2);
+    if (const char* t3 = getenv("CMG_TS3")) P->ts3 = atoi(t3);
+    if (const char* fm = getenv("CMG_FUSE_MASK")) P->fuse_mask = atoi(fm) | 1;
+    if (const char* dg = getenv("CMG_DBG")) P->dbg = atoi(dg);
     auto bail = [&](int rc) {
         cmg_plan_destroy(P);
         return rc;
@@ -534,6 +377,9 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     CKP(cudaMalloc(&P->u, bytes));
     CKP(cudaMalloc(&P->uprev, bytes));
     CKP(cudaMalloc(&P->f, bytes));
+    CKP(cudaMalloc(&P->ubuf[2], bytes));
+    P->ubuf[0] = P->u;
+    P->ubuf[1] = P->uprev;
     size_t maxpad = 0;
     for (int j = 1; j <= layers; ++j) {
         Level& L = P->lv[j];
@@ -562,9 +408,21 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     P->eW = n + 2;
     P->epstride = (long long)P->eH * P->eW;
     if (P->egeneral) CKP(cudaMalloc(&P->epad, P->esz * (size_t)P->epstride * batch));
+    {
+        bool gen = P->egeneral;
+        for (int j = 1; j <= layers; ++j) gen = gen || P->lv[j].general;
+        bool fgen = false;
+        for (int j = 1; j <= std::min(layers, 3); ++j) fgen = fgen || P->lv[j].general;
+        const char* fe = getenv("CMG_FUSED");
+        P->fused = !fgen && !(fe && fe[0] == '0');
+        const char* pe = getenv("CMG_PERSIST");
+        P->persist = !P->fused && !gen && batch <= 1024 && (pe && pe[0] == '1');
+        if (const char* oc = getenv("CMG_OCC")) P->occ_cap = std::max(1, atoi(oc));
+    }
     long long want = std::max(1, 1184 / batch);
     P->nbx = (int)std::max(1LL, std::min(want, (P->N + 255) / 256));
     CKP(cudaMalloc(&P->partials, sizeof(double) * NSUM * (size_t)P->nbx * batch));
+    P->pcap = P->nbx * batch;
     CKP(cudaMalloc(&P->st, sizeof(ImgState) * batch));
     CKP(cudaMalloc(&P->ndone, sizeof(int) * 2));
     P->iters = P->ndone + 1;
@@ -635,7 +493,14 @@ int cmg_sweep_layer(cmg_plan* P, void* u_host, const void* f_host, int layer, do
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
     CK(cudaMemcpyAsync(P->u, u_host, bytes, cudaMemcpyHostToDevice, P->stream));
     CK(cudaMemcpyAsync(P->f, f_host, bytes, cudaMemcpyHostToDevice, P->stream));
-    if (P->dtype == CMG_F64) {
+    void* result = P->u;
+    if (P->fused && layer <= 3 && ((P->fuse_mask >> (layer - 1)) & 1)) {
+        if (P->dtype == CMG_F64)
+            enqueue_fused_level<double>(P, layer, P->u, P->ubuf[2]);
+        else
+            enqueue_fused_level<float>(P, layer, P->u, P->ubuf[2]);
+        result = P->ubuf[2];
+    } else if (P->dtype == CMG_F64) {
         enqueue_fpads<double>(P);
         for (int c = 0; c < 4; ++c) enqueue_sweep<double>(P, layer, c);
     } else {
@@ -645,7 +510,7 @@ int cmg_sweep_layer(cmg_plan* P, void* u_host, const void* f_host, int layer, do
     CK(cudaGetLastError());
     std::vector<ImgState> hs(P->B);
     CK(cudaMemcpyAsync(hs.data(), P->st, sizeof(ImgState) * P->B, cudaMemcpyDeviceToHost, P->stream));
-    CK(cudaMemcpyAsync(u_host, P->u, bytes, cudaMemcpyDeviceToHost, P->stream));
+    CK(cudaMemcpyAsync(u_host, result, bytes, cudaMemcpyDeviceToHost, P->stream));
     CK(cudaStreamSynchronize(P->stream));
     for (int b = 0; b < P->B; ++b)
         if (hs[b].bad) return fail(CMG_ENONFINITE, "corrections must be finite");
@@ -701,6 +566,13 @@ int cmg_time_sweep(cmg_plan* P, int layer, int color, int reps, double* ms_per_l
     if (rc) return rc;
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
     auto one = [&]() {
+        if (P->fused && layer <= 3 && ((P->fuse_mask >> (layer - 1)) & 1)) {  // production fused kernel
+            if (P->dtype == CMG_F64)
+                enqueue_fused_level<double>(P, layer, P->ubuf[0], P->ubuf[2]);
+            else
+                enqueue_fused_level<float>(P, layer, P->ubuf[0], P->ubuf[2]);
+            return;
+        }
         for (int c = (color < 0 ? 0 : color); c <= (color < 0 ? 3 : color); ++c) {
             if (P->dtype == CMG_F64)
                 enqueue_sweep<double>(P, layer, c);

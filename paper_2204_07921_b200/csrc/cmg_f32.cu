@@ -1,0 +1,3 @@
+// float instantiation of the launch sequences
+#include "cmg_launch.cuh"
+CMG_INSTANTIATE(float)

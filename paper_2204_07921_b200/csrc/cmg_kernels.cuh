@@ -65,12 +65,30 @@ struct SweepArgs {
     int flat, single;
     const SolveParams* P;
     ImgState* st;
+    int dbg;  // diagnostics: bit0 skip planes, bit1 skip f*, bit2 skip apply, bit3 exit early
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
+}
+
+// Rare orderings, kept out of line so the hot kernels stay small (I-cache):
+// f* of a colour class with a single patch column (NumPy coalesces the patch
+// into one flat pairwise sum) ...
+template <typename T, int S, class Acc>
+__device__ __noinline__ T fstar_flat_sum(const Acc& U, const Acc& F, int R0, int C0) {
+    using O = X<T>;
+    return O::add(T(0), pairwise_small<T>(S * S, [&](int e) {
+        return O::sub(F(R0 + e / S, C0 + e % S), U(R0 + e / S, C0 + e % S));
+    }));
+}
+// ... and the plane mean of a colour class holding a single patch
+// (d.mean(axis=0) on a (iota,1,1) array is pairwise, not sequential).
+template <typename T>
+__device__ __noinline__ T pairwise_of(const T* v, int n) {
+    return pairwise_any<T>(n, [&](int i) { return v[i]; });
 }
 
 // ---------------------------------------------------------------------------
@@ -92,7 +110,7 @@ __device__ __forceinline__ T patch_solve_ct(const Acc& U, const Acc& F, int R0, 
         auto D = [&](int aa, int bb) { return O::sub(F(R0 + aa, C0 + bb), U(R0 + aa, C0 + bb)); };
         T acc;
         if (a.flat) {
-            acc = O::add(T(0), pairwise_small<T>(S * S, [&](int e) { return D(e / S, e % S); }));
+            acc = fstar_flat_sum<T, S>(U, F, R0, C0);
         } else {
             acc = T(0);
 #pragma unroll
@@ -113,7 +131,7 @@ __device__ __forceinline__ T patch_solve_ct(const Acc& U, const Acc& F, int R0, 
             static_for<0, NPL>([&](auto l) { plane_exact<T, decltype(l)::value>(U, ci, cc, uo, &d[decltype(l)::value], nullptr); });
             T sum;
             if (a.single) {
-                sum = pairwise_small<T>(NPL, [&](int i) { return d[i]; });
+                sum = pairwise_of<T>(d, NPL);
             } else {
                 sum = d[0];
 #pragma unroll
@@ -167,6 +185,13 @@ __device__ __forceinline__ void apply_patch(T* u, int m, int n, int R0, int C0, 
         }
 }
 
+// Border patches (odd reflection) take an out-of-line copy of the solve.
+template <typename T, int LAYER, int MODE, int PREC>
+__device__ __noinline__ T patch_solve_ct_border(const T* u, const T* f, int R0, int C0, const SweepArgs<T>& a) {
+    Reflect<T> U{u, a.m, a.n}, F{f, a.m, a.n};
+    return patch_solve_ct<T, LAYER, MODE, PREC>(U, F, R0, C0, a);
+}
+
 template <typename T, int LAYER, int MODE, int PREC, int SRC>
 __global__ void __launch_bounds__(256) k_sweep_tpp(SweepArgs<T> a) {
     const int b = blockIdx.z;
@@ -188,12 +213,198 @@ __global__ void __launch_bounds__(256) k_sweep_tpp(SweepArgs<T> a) {
             Direct<T> U{u, a.n}, F{f, a.n};
             c = patch_solve_ct<T, LAYER, MODE, PREC>(U, F, R0, C0, a);
         } else {
-            Reflect<T> U{u, a.m, a.n}, F{f, a.m, a.n};
-            c = patch_solve_ct<T, LAYER, MODE, PREC>(U, F, R0, C0, a);
+            c = patch_solve_ct_border<T, LAYER, MODE, PREC>(u, f, R0, C0, a);
         }
     }
     if (!isfinite(c)) a.st[b].bad = 1;
     apply_patch(u, a.m, a.n, R0, C0, S, c);
+}
+
+
+// ---------------------------------------------------------------------------
+// Team-per-patch sweep (levels 2-3): TS consecutive lanes of a warp cooperate
+// on one patch -- rows of f* in parallel, planes split across lanes, the
+// NumPy-ordered reductions replayed through warp shuffles.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct ArgBest {
+    T v;
+    int i;
+    bool nan;
+};
+
+// np.argmin / np.argmax order: any NaN beats numbers (first NaN index wins),
+// otherwise strictly better value, ties -> smaller index.
+template <bool MIN, typename T>
+__device__ __forceinline__ ArgBest<T> arg_better(const ArgBest<T>& a, const ArgBest<T>& b) {
+    if (a.nan || b.nan) {
+        if (a.nan && b.nan) return a.i <= b.i ? a : b;
+        return a.nan ? a : b;
+    }
+    if (MIN ? (a.v < b.v) : (a.v > b.v)) return a;
+    if (MIN ? (b.v < a.v) : (b.v > a.v)) return b;
+    return a.i <= b.i ? a : b;
+}
+
+template <bool MIN, int TS, typename T>
+__device__ __forceinline__ ArgBest<T> arg_reduce(ArgBest<T> x) {
+#pragma unroll
+    for (int o = TS / 2; o > 0; o >>= 1) {
+        ArgBest<T> y;
+        y.v = __shfl_xor_sync(0xffffffffu, x.v, o, TS);
+        y.i = __shfl_xor_sync(0xffffffffu, x.i, o, TS);
+        y.nan = __shfl_xor_sync(0xffffffffu, (int)x.nan, o, TS) != 0;
+        x = arg_better<MIN>(x, y);
+    }
+    return x;
+}
+
+template <typename T, int LAYER, int MODE, int PREC, int TS, class Acc>
+__device__ __forceinline__ T patch_solve_team(const Acc& U, const Acc& F, int R0, int C0, int lane,
+                                              const SweepArgs<T>& a) {
+    using O = X<T>;
+    constexpr int S = (1 << LAYER) - 1;
+    constexpr int R = 1 << (LAYER - 1);
+    constexpr int NPL = 1 << (LAYER + 2);
+    constexpr unsigned FULL = 0xffffffffu;
+    static_assert(TS >= S && TS <= 32 && (32 % TS) == 0, "team size");
+    const int ci = R0 + R - 1, cc = C0 + R - 1;
+    auto D = [&](int aa, int bb) { return O::sub(F(R0 + aa, C0 + bb), U(R0 + aa, C0 + bb)); };
+
+    // f*: lane t owns row t (driver.py:244-246; rows sequential, each pairwise)
+    T rowsum = T(0);
+    if (a.dbg & 2) {
+    } else if (a.flat) {
+        if (lane == 0) rowsum = fstar_flat_sum<T, S>(U, F, R0, C0);
+    } else if (lane < S) {
+        rowsum = pairwise_small<T>(S, [&](int bb) { return D(lane, bb); });
+    }
+    T acc;
+    if (a.flat) {
+        acc = __shfl_sync(FULL, rowsum, 0, TS);
+    } else {
+        acc = T(0);
+#pragma unroll
+        for (int aa = 0; aa < S; ++aa) acc = O::add(acc, __shfl_sync(FULL, rowsum, aa, TS));
+    }
+    const T fstar = O::div(acc, T(S * S));
+
+    const T uo = U(ci, cc);
+    T chalf;
+    if (a.dbg & 1) {
+        chalf = uo;
+    } else if constexpr (MODE == MODE_MEAN && PREC == PREC_FAST) {
+        constexpr int NPAIR = NPL / 2;
+        T part = T(0);
+#pragma unroll
+        for (int k = 0; k < (NPAIR + TS - 1) / TS; ++k) {
+            const int pi = lane + k * TS;
+            if (pi < NPAIR) {
+                const PlaneRT pl = PlaneRT::getg(2 * pi);
+                const int Lq = pl.x0 * pl.x0 + pl.x1 * pl.x1;
+                const T up = U(ci + pl.x0, cc + pl.x1), um = U(ci - pl.x0, cc - pl.x1);
+                const T uq = U(ci + pl.y0, cc + pl.y1), umq = U(ci - pl.y0, cc - pl.y1);
+                const T sp = up + um;
+                const T N = sp - T(2) * uo;
+                const T Dd = up - um;
+                const T base = Dd * Dd + T(4 * Lq);
+                const T Sa = sp - T(2) * uq, Sb = sp - T(2) * umq;
+                part += (sqrt(T(Lq)) * N) * (frsqrt(Sa * Sa + base) + frsqrt(Sb * Sb + base));
+            }
+        }
+#pragma unroll
+        for (int o = TS / 2; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o, TS);
+        chalf = part * T(1.0 / NPL);
+    } else if constexpr (MODE == MODE_MEAN) {
+        constexpr int PPL = NPL / TS;
+        T d[PPL];
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) plane_exact_rt<T>(U, ci, cc, uo, PlaneRT::getg(lane + k * TS), &d[k], nullptr);
+        T sum;
+        if (a.single) {
+            T all[NPL];
+#pragma unroll
+            for (int l = 0; l < NPL; ++l) all[l] = __shfl_sync(FULL, d[l / TS], l % TS, TS);
+            sum = pairwise_of<T>(all, NPL);
+        } else {
+            sum = __shfl_sync(FULL, d[0], 0, TS);
+#pragma unroll
+            for (int l = 1; l < NPL; ++l) sum = O::add(sum, __shfl_sync(FULL, d[l / TS], l % TS, TS));
+        }
+        chalf = O::div(sum, T(NPL));
+    } else {
+        constexpr int PPL = NPL / TS;
+        ArgBest<T> bmin, bmax;
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) {
+            T v;
+            plane_exact_rt<T>(U, ci, cc, uo, PlaneRT::getg(lane + k * TS), nullptr, &v);
+            ArgBest<T> c{v, lane + k * TS, (bool)isnan(v)};
+            if (k == 0) {
+                bmin = c;
+                bmax = c;
+            } else {
+                bmin = arg_better<true>(bmin, c);
+                bmax = arg_better<false>(bmax, c);
+            }
+        }
+        bmin = arg_reduce<true, TS>(bmin);
+        bmax = arg_reduce<false, TS>(bmax);
+        const int star = (fabs(bmin.v) <= fabs(bmax.v)) ? bmin.i : bmax.i;
+        T ph = T(0);
+        if (lane == 0) plane_exact_rt<T>(U, ci, cc, uo, PlaneRT::getg(star), &ph, nullptr);
+        chalf = __shfl_sync(FULL, ph, 0, TS);
+    }
+    T c = T(0);
+    for (int t = 0; t < a.P->inner; ++t)
+        c = O::div(O::add(O::add(c, chalf), O::mul(T(a.P->w[LAYER][t]), fstar)), T(a.P->den[LAYER][t]));
+    return c;
+}
+
+template <typename T, int LAYER, int MODE, int PREC, int TS>
+__device__ __noinline__ T patch_solve_team_border(const T* u, const T* f, int R0, int C0, int lane,
+                                                  const SweepArgs<T>& a) {
+    Reflect<T> U{u, a.m, a.n}, F{f, a.m, a.n};
+    return patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, a);
+}
+
+template <typename T, int LAYER, int MODE, int PREC, int SRC, int TS>
+__global__ void __launch_bounds__(256) k_sweep_team(SweepArgs<T> a) {
+    const int b = blockIdx.z;
+    if (a.st[b].done) return;  // uniform per block
+    constexpr int S = (1 << LAYER) - 1;
+    const int lane = threadIdx.x % TS;
+    const long long npatch = (long long)a.hc * a.wc;
+    long long idx = (long long)blockIdx.x * (blockDim.x / TS) + threadIdx.x / TS;
+    const bool valid = idx < npatch;
+    if (!valid) idx = npatch - 1;  // keep the whole warp converged for the shuffles
+    const int pr = (int)(idx / a.wc), pc = (int)(idx % a.wc);
+    const int R0 = (2 * pr + a.p) * S, C0 = (2 * pc + a.q) * S;
+    T* u = a.u + (long long)b * a.istride;
+    const T* f = a.f + (long long)b * a.istride;
+    if (a.dbg & 8) return;
+    T c;
+    if constexpr (SRC == SRC_PADDED) {
+        Padded<T> U{a.upad + (long long)b * a.pstride, a.W}, F{a.fpad + (long long)b * a.pstride, a.W};
+        c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, a);
+    } else {
+        const bool inside = (R0 >= 1) && (C0 >= 1) && (R0 + S < a.m) && (C0 + S < a.n);
+        if (__all_sync(0xffffffffu, inside)) {
+            Direct<T> U{u, a.n}, F{f, a.n};
+            c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, a);
+        } else {
+            c = patch_solve_team_border<T, LAYER, MODE, PREC, TS>(u, f, R0, C0, lane, a);
+        }
+    }
+    if (!valid || (a.dbg & 4)) return;
+    if (lane == 0 && !isfinite(c)) a.st[b].bad = 1;
+    for (int e = lane; e < S * S; e += TS) {
+        const int i = R0 + e / S, k = C0 + e % S;
+        if (i < a.m && k < a.n) {
+            T* p = u + (long long)i * a.n + k;
+            *p = X<T>::add(*p, c);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -412,7 +623,7 @@ struct TraceArgs {
 
 // One CTA per image: reduce partials in a fixed order, record the trace and
 // apply the stopping rule (driver.py:294-310).
-__global__ void __launch_bounds__(256) k_finalize(const double* partials, int nbx, const SolveParams* P,
+static __global__ void __launch_bounds__(256) k_finalize(const double* partials, int nbx, const SolveParams* P,
                                                   ImgState* st, TraceArgs tr, int initial) {
     const int b = blockIdx.x;
     ImgState& S = st[b];

@@ -1,0 +1,388 @@
+// cmg_launch.cuh -- kernel launch sequences per element type (instantiated in
+// cmg_f64.cu / cmg_f32.cu so the two dtypes compile in parallel).
+#pragma once
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "cmg_fused.cuh"
+#include "cmg_persist.cuh"
+#include "cmg_plan.h"
+
+namespace cmg {
+
+template <typename T>
+void enqueue_pad(cmg_plan* P, const void* src, void* dst, int H, int W, long long pstride, int bot, int rgt,
+                 bool gate) {
+    const ImgState* st = gate ? P->st : nullptr;
+    const int blocks = (int)std::min<long long>((P->N + 255) / 256, 4096);
+    k_pad_copy<T><<<dim3(blocks, P->B), 256, 0, P->stream>>>((const T*)src, P->N, (T*)dst, pstride, P->m, P->n, W,
+                                                             st);
+    k_pad_axis<T><<<dim3((P->n + 127) / 128, P->B), 128, 0, P->stream>>>((T*)dst, pstride, 0, P->m, P->n, H, W,
+                                                                         bot, rgt, st);
+    k_pad_axis<T><<<dim3((H + 127) / 128, P->B), 128, 0, P->stream>>>((T*)dst, pstride, 1, P->m, P->n, H, W, bot,
+                                                                      rgt, st);
+    P->enq += 3;
+}
+
+template <typename T, int LAYER, int MODE, int PREC>
+void launch_tpp(const SweepArgs<T>& a, bool padded, int B, cudaStream_t s) {
+    const dim3 blk(32, 8);
+    const dim3 grd((a.wc + 31) / 32, (a.hc + 7) / 8, B);
+    if (padded)
+        k_sweep_tpp<T, LAYER, MODE, PREC, SRC_PADDED><<<grd, blk, 0, s>>>(a);
+    else
+        k_sweep_tpp<T, LAYER, MODE, PREC, SRC_INPLACE><<<grd, blk, 0, s>>>(a);
+}
+
+template <typename T, int LAYER, int MODE, int PREC, int TS>
+void launch_team(const SweepArgs<T>& a, bool padded, int B, cudaStream_t s) {
+    const long long np = (long long)a.hc * a.wc;
+    const int per_block = 256 / TS;
+    const dim3 grd((unsigned)((np + per_block - 1) / per_block), 1, B);
+    if (padded)
+        k_sweep_team<T, LAYER, MODE, PREC, SRC_PADDED, TS><<<grd, 256, 0, s>>>(a);
+    else
+        k_sweep_team<T, LAYER, MODE, PREC, SRC_INPLACE, TS><<<grd, 256, 0, s>>>(a);
+}
+
+template <typename T, int MODE, int PREC>
+void dispatch_small_layer(const cmg_plan* P, const SweepArgs<T>& a, bool padded) {
+    switch (a.layer) {
+        case 1: launch_tpp<T, 1, MODE, PREC>(a, padded, P->B, P->stream); break;
+        case 2:
+            if (P->ts2 == 16)
+                launch_team<T, 2, MODE, PREC, 16>(a, padded, P->B, P->stream);
+            else if (P->ts2 == 8)
+                launch_team<T, 2, MODE, PREC, 8>(a, padded, P->B, P->stream);
+            else
+                launch_team<T, 2, MODE, PREC, 4>(a, padded, P->B, P->stream);
+            break;
+        default:
+            if (P->ts3 == 32)
+                launch_team<T, 3, MODE, PREC, 32>(a, padded, P->B, P->stream);
+            else if (P->ts3 == 16)
+                launch_team<T, 3, MODE, PREC, 16>(a, padded, P->B, P->stream);
+            else
+                launch_team<T, 3, MODE, PREC, 8>(a, padded, P->B, P->stream);
+            break;
+    }
+}
+
+template <typename T>
+void enqueue_sweep(cmg_plan* P, int layer, int color) {
+    Level& L = P->lv[layer];
+    const int p = color >> 1, q = color & 1;
+    const int hc = (L.mj - p + 1) / 2, wc = (L.nj - q + 1) / 2;
+    if (hc <= 0 || wc <= 0) return;
+    if (L.general) enqueue_pad<T>(P, P->u, P->upad, L.H, L.W, L.pstride, 1 + L.mp - P->m, 1 + L.np - P->n, true);
+    SweepArgs<T> a;
+    a.u = (T*)P->u;
+    a.f = (const T*)P->f;
+    a.istride = P->N;
+    a.upad = (const T*)P->upad;
+    a.fpad = (const T*)L.fpad;
+    a.pstride = L.pstride;
+    a.W = L.W;
+    a.m = P->m;
+    a.n = P->n;
+    a.layer = layer;
+    a.s = L.s;
+    a.r = L.r;
+    a.p = p;
+    a.q = q;
+    a.hc = hc;
+    a.wc = wc;
+    a.flat = (wc == 1);      // NumPy coalesces a single patch column
+    a.single = (hc * wc == 1);  // single patch: d.mean(axis=0) becomes pairwise
+    a.P = P->P;
+    a.st = P->st;
+    a.dbg = P->dbg;
+    const bool padded = L.general;
+    if (layer <= 3) {
+        if (P->mode == CMG_MODE_GAUSS)
+            dispatch_small_layer<T, MODE_GAUSS, PREC_EXACT>(P, a, padded);
+        else if (P->prec == CMG_PREC_FAST)
+            dispatch_small_layer<T, MODE_MEAN, PREC_FAST>(P, a, padded);
+        else
+            dispatch_small_layer<T, MODE_MEAN, PREC_EXACT>(P, a, padded);
+    } else {
+        const dim3 grd(wc, hc, P->B);
+        if (P->mode == CMG_MODE_GAUSS) {
+            if (padded)
+                k_sweep_bpp<T, MODE_GAUSS, SRC_PADDED><<<grd, 128, 0, P->stream>>>(a);
+            else
+                k_sweep_bpp<T, MODE_GAUSS, SRC_INPLACE><<<grd, 128, 0, P->stream>>>(a);
+        } else {
+            if (padded)
+                k_sweep_bpp<T, MODE_MEAN, SRC_PADDED><<<grd, 128, 0, P->stream>>>(a);
+            else
+                k_sweep_bpp<T, MODE_MEAN, SRC_INPLACE><<<grd, 128, 0, P->stream>>>(a);
+        }
+    }
+    P->enq += 1;
+}
+
+template <typename T>
+__global__ void k_copy(const T* __restrict__ src, T* __restrict__ dst, long long N, const ImgState* st) {
+    const int b = blockIdx.y;
+    if (st[b].done) return;
+    const long long off = (long long)b * N;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (long long)gridDim.x * blockDim.x)
+        dst[off + e] = src[off + e];
+}
+
+template <typename T>
+void enqueue_copy_prev(cmg_plan* P) {
+    const int blocks = (int)std::min<long long>((P->N + 255) / 256, 2048);
+    k_copy<T><<<dim3(blocks, P->B), 256, 0, P->stream>>>((const T*)P->u, (T*)P->uprev, P->N, P->st);
+    P->enq += 1;
+}
+
+template <typename T>
+void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has_ref, double* eonly, int initial) {
+    if (P->egeneral) enqueue_pad<T>(P, u, P->epad, P->eH, P->eW, P->epstride, 1, 1, !initial && !eonly);
+    EnergyArgs ea;
+    ea.u = u;
+    ea.f = P->f;
+    ea.uprev = uprev;
+    ea.ref = has_ref ? P->ref : nullptr;
+    ea.upad = P->epad;
+    ea.istride = P->N;
+    ea.pstride = P->epstride;
+    ea.m = P->m;
+    ea.n = P->n;
+    ea.W = P->eW;
+    ea.mode = P->mode;
+    ea.nbx = P->nbx;
+    ea.partials = P->partials;
+    ea.st = P->st;
+    if (P->egeneral)
+        k_energy<T, SRC_PADDED><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea);
+    else
+        k_energy<T, SRC_INPLACE><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea);
+    TraceArgs ta;
+    ta.energy = P->tr[0];
+    ta.rel_e = P->tr[1];
+    ta.rel_u = P->tr[2];
+    ta.psnr = P->tr[3];
+    ta.seconds = P->tr[4];
+    ta.cap = P->cap;
+    ta.ndone = P->ndone;
+    ta.eonly = eonly;
+    k_finalize<<<P->B, 256, 0, P->stream>>>(P->partials, P->nbx, P->P, P->st, ta, initial);
+    P->enq += 2;
+}
+
+template <typename T>
+void enqueue_energy(cmg_plan* P, bool has_ref, double* eonly, int initial) {
+    enqueue_energy_ptrs<T>(P, P->u, P->uprev, has_ref, eonly, initial);
+}
+
+// tile sizes (patches per tile side) and lanes per patch of the fused levels
+template <int LAYER>
+struct FusedCfg;
+template <>
+struct FusedCfg<1> {
+    static constexpr int TP = 32, TS = 1;
+};
+template <>
+struct FusedCfg<2> {
+    static constexpr int TP = 8, TS = 4;
+};
+template <>
+struct FusedCfg<3> {
+    static constexpr int TP = 4, TS = 8;
+};
+
+template <typename T, int LAYER, int MODE, int PREC>
+void launch_fused(cmg_plan* P, const FusedArgs<T>& a, int tiles) {
+    constexpr int TP = FusedCfg<LAYER>::TP, TS = FusedCfg<LAYER>::TS;
+    constexpr int RD = FusedGeom<LAYER, TP>::RD;
+    const size_t smem = 2 * sizeof(T) * RD * RD;
+    auto kern = k_level_fused<T, LAYER, MODE, PREC, TP, TS>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    kern<<<dim3(tiles, 1, P->B), 256, smem, P->stream>>>(a);
+}
+
+template <typename T, int MODE, int PREC>
+void dispatch_fused(cmg_plan* P, int layer, const FusedArgs<T>& a, int tiles) {
+    if (layer == 1)
+        launch_fused<T, 1, MODE, PREC>(P, a, tiles);
+    else if (layer == 2)
+        launch_fused<T, 2, MODE, PREC>(P, a, tiles);
+    else
+        launch_fused<T, 3, MODE, PREC>(P, a, tiles);
+}
+
+inline int fused_tp(int layer) { return layer == 1 ? FusedCfg<1>::TP : layer == 2 ? FusedCfg<2>::TP : FusedCfg<3>::TP; }
+
+template <typename T>
+void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
+    const Level& L = P->lv[layer];
+    FusedArgs<T> a;
+    a.uin = (const T*)uin;
+    a.uout = (T*)uout;
+    a.f = (const T*)P->f;
+    a.istride = P->N;
+    a.m = P->m;
+    a.n = P->n;
+    a.mj = L.mj;
+    a.nj = L.nj;
+    const int TP = fused_tp(layer);
+    const int tiles_r = (L.mj + TP - 1) / TP;
+    a.tiles_c = (L.nj + TP - 1) / TP;
+    for (int c = 0; c < 4; ++c) {
+        const int p = c >> 1, q = c & 1;
+        a.hc[c] = (L.mj - p + 1) / 2;
+        a.wc[c] = (L.nj - q + 1) / 2;
+    }
+    a.P = P->P;
+    a.st = P->st;
+    const int tiles = tiles_r * a.tiles_c;
+    if (P->mode == CMG_MODE_GAUSS)
+        dispatch_fused<T, MODE_GAUSS, PREC_EXACT>(P, layer, a, tiles);
+    else if (P->prec == CMG_PREC_FAST)
+        dispatch_fused<T, MODE_MEAN, PREC_FAST>(P, layer, a, tiles);
+    else
+        dispatch_fused<T, MODE_MEAN, PREC_EXACT>(P, layer, a, tiles);
+    P->enq += 1;
+}
+
+// Two V-cycles per graph body with a 3-buffer rotation: fused levels write
+// into a buffer that is neither their input nor the cycle's u_prev, so rel_u
+// needs no copy, and after the two cycles u is back in ubuf[0].
+template <typename T>
+void enqueue_body_fused(cmg_plan* P, int full, bool has_ref) {
+    std::vector<int> seq;
+    for (int j = 1; j <= P->layers; ++j) seq.push_back(j);
+    if (full)
+        for (int j = P->layers - 1; j >= 1; --j) seq.push_back(j);
+    auto fusedj = [&](int j) { return j <= 3 && ((P->fuse_mask >> (j - 1)) & 1); };
+    int nf = 0;
+    for (int j : seq) nf += fusedj(j);
+    int cur = 0;
+    for (int half = 0; half < 2; ++half) {
+        const int prev = cur;
+        const int target = (half == 0) ? 1 : 0;
+        int other = 3 - prev - target;
+        bool first = true;
+        for (int j : seq) {
+            if (fusedj(j)) {
+                int out;
+                if (first) {
+                    out = (nf & 1) ? target : other;
+                    first = false;
+                } else {
+                    out = 3 - prev - cur;
+                }
+                enqueue_fused_level<T>(P, j, P->ubuf[cur], P->ubuf[out]);
+                cur = out;
+            } else {
+                void* save = P->u;
+                P->u = P->ubuf[cur];
+                for (int c = 0; c < 4; ++c) enqueue_sweep<T>(P, j, c);
+                P->u = save;
+            }
+        }
+        enqueue_energy_ptrs<T>(P, P->ubuf[cur], P->ubuf[prev], has_ref, nullptr, 0);
+    }
+}
+
+template <typename T>
+void enqueue_fpads(cmg_plan* P) {
+    for (int j = 1; j <= P->layers; ++j) {
+        Level& L = P->lv[j];
+        if (L.general) enqueue_pad<T>(P, P->f, L.fpad, L.H, L.W, L.pstride, 1 + L.mp - P->m, 1 + L.np - P->n, false);
+    }
+}
+
+template <typename T, int MODE, int PREC>
+cudaError_t persist_launch_v(cmg_plan* P, bool has_ref, int full) {
+    auto kern = k_persist<T, MODE, PREC, 4, 16>;
+    PersistArgs a;
+    memset(&a, 0, sizeof(a));
+    a.u = P->u;
+    a.uprev = P->uprev;
+    a.f = P->f;
+    a.ref = has_ref ? P->ref : nullptr;
+    a.has_ref = has_ref ? 1 : 0;
+    a.N = P->N;
+    a.m = P->m;
+    a.n = P->n;
+    a.B = P->B;
+    a.nseq = 0;
+    for (int j = 1; j <= P->layers; ++j) a.seq[a.nseq++] = j;
+    if (full)
+        for (int j = P->layers - 1; j >= 1; --j) a.seq[a.nseq++] = j;
+    for (int j = 1; j <= P->layers; ++j) {
+        const Level& L = P->lv[j];
+        a.side[j] = L.s;
+        for (int c = 0; c < 4; ++c) {
+            const int p = c >> 1, q = c & 1;
+            a.hc[j][c] = (L.mj - p + 1) / 2;
+            a.wc[j][c] = (L.nj - q + 1) / 2;
+        }
+    }
+    a.P = P->P;
+    a.st = P->st;
+    a.tr.energy = P->tr[0];
+    a.tr.rel_e = P->tr[1];
+    a.tr.rel_u = P->tr[2];
+    a.tr.psnr = P->tr[3];
+    a.tr.seconds = P->tr[4];
+    a.tr.cap = P->cap;
+    a.tr.ndone = P->ndone;
+    a.tr.eonly = nullptr;
+    const size_t smem = sizeof(double) * P->B + sizeof(int) * ((P->B + 1) & ~1) + sizeof(double) * NSUM * 32 +
+                        sizeof(T) * (64 + 256 + 2);
+    cudaError_t e;
+    if (P->pgrid == 0) {
+        int nb = 0, dev = 0, nsm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 256, smem);
+        if (e != cudaSuccess) return e;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (nb < 1) return cudaErrorCooperativeLaunchTooLarge;
+        P->pgrid = nsm * std::min(nb, P->occ_cap);
+    }
+    a.npieces = std::max(1, P->pgrid / P->B);
+    a.piece = (P->N + a.npieces - 1) / a.npieces;
+    a.npieces = (int)((P->N + a.piece - 1) / a.piece);
+    const int need = a.npieces * P->B;
+    if (need > P->pcap) {
+        if (P->partials) cudaFree(P->partials);
+        e = cudaMalloc(&P->partials, sizeof(double) * NSUM * (size_t)need);
+        if (e != cudaSuccess) return e;
+        P->pcap = need;
+    }
+    a.partials = P->partials;
+    void* args[] = {&a};
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(P->pgrid), dim3(256), args, smem, P->stream);
+    P->enq += 1;
+    return e;
+}
+
+template <typename T>
+cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full) {
+    if (P->mode == CMG_MODE_GAUSS) return persist_launch_v<T, MODE_GAUSS, PREC_EXACT>(P, has_ref, full);
+    if (P->prec == CMG_PREC_FAST) return persist_launch_v<T, MODE_MEAN, PREC_FAST>(P, has_ref, full);
+    return persist_launch_v<T, MODE_MEAN, PREC_EXACT>(P, has_ref, full);
+}
+
+}  // namespace cmg
+
+#define CMG_INSTANTIATE(T)                                                          \
+    template void cmg::enqueue_sweep<T>(cmg_plan*, int, int);                       \
+    template void cmg::enqueue_energy<T>(cmg_plan*, bool, double*, int);            \
+    template void cmg::enqueue_copy_prev<T>(cmg_plan*);                             \
+    template void cmg::enqueue_fpads<T>(cmg_plan*);                             \
+    template cudaError_t cmg::persist_launch<T>(cmg_plan*, bool, int);               \
+    template void cmg::enqueue_fused_level<T>(cmg_plan*, int, const void*, void*);  \
+    template void cmg::enqueue_energy_ptrs<T>(cmg_plan*, const void*, const void*, bool, double*, int); \
+    template void cmg::enqueue_body_fused<T>(cmg_plan*, int, bool);

@@ -1,0 +1,85 @@
+// cmg_plan.h -- the solver plan (device buffers, graph, statistics) shared by
+// the host runtime (cmg.cu) and the per-dtype launch units (cmg_f64/f32.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../../include/cmg.h"
+#include "cmg_kernels.cuh"
+
+namespace cmg {
+
+// One level of the hierarchy (hierarchy.Partition, hierarchy.py:29-73).
+struct Level {
+    int layer = 0, s = 0, r = 0, mj = 0, nj = 0, mp = 0, np = 0;
+    bool general = false;  // needs numpy's iterated/singleton reflection -> padded snapshot
+    int H = 0, W = 0;
+    long long pstride = 0;
+    void* fpad = nullptr;
+};
+
+}  // namespace cmg
+
+struct cmg_plan {
+    int m = 0, n = 0, B = 0, layers = 0, mode = 0, dtype = 0, prec = 0, device = 0;
+    size_t esz = 8;
+    long long N = 0;
+    cudaStream_t stream = nullptr;
+    void *u = nullptr, *uprev = nullptr, *f = nullptr, *ref = nullptr, *upad = nullptr, *epad = nullptr;
+    size_t upad_elems = 0;
+    bool egeneral = false;
+    int eH = 0, eW = 0;
+    long long epstride = 0;
+    cmg::Level lv[7];
+    double* partials = nullptr;
+    int nbx = 1;
+    cmg::ImgState* st = nullptr;
+    int* ndone = nullptr;
+    int* iters = nullptr;
+    double* eonly = nullptr;
+    cmg::SolveParams* P = nullptr;
+    double* tr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    int cap = 0;
+    // kernel variants
+    int ts2 = 4, ts3 = 16;
+    int dbg = 0;  // diagnostics bits (CMG_DBG), see SweepArgs::dbg  // team sizes (lanes per patch) of levels 2 and 3
+    // graphs
+    cudaGraphExec_t exec = nullptr;
+    int gkey = -1;
+    bool use_while = true;
+    int nodes_per_cycle = 0;
+    // stats
+    long long launches = 0;
+    int cycles_run = 0;
+    float dev_ms = 0.f;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int enq = 0;  // kernels enqueued since last reset
+    // fused-level path (all four colours of a level in one tile kernel)
+    bool fused = false;
+    int fuse_mask = 1;  // bit j-1: level j runs as one fused tile kernel (bit 0 required)
+    void* ubuf[3] = {nullptr, nullptr, nullptr};  // rotation buffers (ubuf[0]=u, ubuf[1]=uprev)
+    // persistent cooperative path
+    bool persist = false;
+    int pgrid = 0;          // CTAs of the persistent kernel
+    int pcap = 0;           // partials capacity (images*pieces)
+    int occ_cap = 4;        // max CTAs per SM for the persistent kernel
+};
+
+namespace cmg {
+template <typename T>
+void enqueue_sweep(cmg_plan* P, int layer, int color);
+template <typename T>
+void enqueue_energy(cmg_plan* P, bool has_ref, double* eonly, int initial);
+template <typename T>
+void enqueue_copy_prev(cmg_plan* P);
+template <typename T>
+void enqueue_fpads(cmg_plan* P);
+template <typename T>
+cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full);
+template <typename T>
+void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout);
+template <typename T>
+void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has_ref, double* eonly, int initial);
+template <typename T>
+void enqueue_body_fused(cmg_plan* P, int full, bool has_ref);
+}  // namespace cmg
