@@ -1,23 +1,27 @@
 """Benchmark: the BASELINE metric on the B200 hot path.
 
-Workload (BASELINE.json configs[2], the metric's "1024^2 time-to-tolerance"):
-mean-curvature denoising of the seeded 1024x1024 synthetic image (32 shapes +
-texture, sigma 25/255), J=3 levels, alpha=0.06, epsilon=1e-6 (40 V-cycles, as
-the reference).  One STEP = one complete denoise to tolerance.
+Default workload (BASELINE.json configs[2] -- the metric's "1024^2
+time-to-tolerance"): mean-curvature denoising of the seeded 1024x1024 image
+(32 shapes + texture, sigma 25/255), J=3, alpha=0.06, epsilon=1e-6 (40 V-cycles,
+as the reference), float64 with the exact (bit-identical) arithmetic.  One STEP
+= one complete denoise to tolerance.  Metric: pixel-sweeps per second (a
+pixel-sweep = one pixel relaxed by one level's four-colour pass).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--dtype float64|float32] [--precision exact|fast] [--config 3]
+                    [--config 3|4|5] [--dtype float64|float32] [--precision exact|fast]
 
-Prints one JSON line (rank 0).  Under torchrun (N>1) every rank solves its own
-replica (the image does not shard: "replicas only", weak scaling); value is
-the total over ranks divided by the max-over-ranks time.
+Multi-GPU (torchrun, one rank per GPU):
+  config 3  one image does not shard -> replicas (weak scaling);
+  config 4  64 x 512^2 fp32 images, 20 cycles, images sharded over ranks;
+  config 5  16384^2 fp32, 10 cycles, horizontal strips with NCCL ghost-row
+            exchange after every level (paper_2204_07921_b200.strips).
 """
 
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -38,7 +42,7 @@ def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
@@ -101,40 +105,57 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_sample(f, layers, cycles, threads):
-    """Oracle (port of the reference algorithm) on a bounded sample; returns Mpx-sweeps/s."""
+def workload(cfgid: int, dtype: str, prec: str):
+    from paper_2204_07921_b200 import synth
+
+    c = synth.CONFIGS[cfgid]
+    size, layers = c["size"], c["layers"]
+    eps = c.get("eps", 1e-300)
+    batch = c.get("batch", 1)
+    desc = {1: "256^2 MC, J=6, 10 cycles", 2: "512^2 GC, J=6, eps 1e-6 / 50 cycles",
+            3: "1024^2 MC to eps 1e-6, J=3", 4: "64 x 512^2 MC, J=3, 20 cycles",
+            5: "16384^2 MC, J=3, 10 cycles"}[cfgid]
+    return c, size, layers, eps, batch, f"config{cfgid}: {desc}, alpha=0.06, {dtype}, precision={prec}"
+
+
+def cpu_sample(f, layers, cycles, threads, mode="mean"):
+    """The oracle (C port of the reference algorithm) on a bounded sample."""
     from oracle import oracle as O
 
     t = time.perf_counter()
-    r = O.denoise(f, mode="mean", layers=layers, max_outer=cycles, epsilon=1e-300, threads=threads)
+    O.denoise(f, mode=mode, layers=layers, max_outer=cycles, epsilon=1e-300, threads=threads)
     dt = time.perf_counter() - t
     m, n = f.shape
-    return cycles * layers * m * n / dt / 1e6, dt, r
+    return cycles * layers * m * n / dt / 1e6, dt
 
 
 def run_reference(args):
+    """Reference arm: the reference algorithm on the host cores (oracle port,
+    all threads), same workload / metric / unit, bounded sample per step."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     from oracle import oracle as O
     from paper_2204_07921_b200 import synth
 
+    c, size, layers, eps, batch, desc = workload(args.config, args.dtype, args.precision)
     f, _ = synth.config_input(args.config, 0, fp32=(args.dtype == "float32"))
-    layers = synth.CONFIGS[args.config]["layers"]
+    if args.config == 5:  # bounded sample: a 2048-row band of the image
+        f = f[:2048]
     threads = O.max_threads()
     cycles = args.ref_cycles
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_sample(f, layers, 1, threads)
+    cpu_sample(f, layers, 1, threads, c["mode"])  # warm-up
     vals, times = [], []
     for _ in range(args.steps):
-        v, dt, _ = cpu_sample(f, layers, cycles, threads)
+        v, dt = cpu_sample(f, layers, cycles, threads, c["mode"])
         vals.append(v)
         times.append(dt)
     value = float(np.mean(vals))
-    m, n = f.shape
+    sample = (f"{cycles} V-cycles of {f.shape[0]}x{f.shape[1]} ({desc}) per step; oracle/cmg_oracle.c "
+              f"(C restatement of the reference NumPy algorithm), OpenMP over patches, {threads} threads")
     line = {
         "impl": "reference",
-        "metric": "Mpixel-sweeps/s (1024^2 MC denoise, J=3)",
+        "metric": "Mpixel-sweeps/s",
         "value": value,
         "unit": "Mpixel-sweeps/s",
         "n_gpus": args.gpus,
@@ -146,165 +167,264 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (BASELINE seeded generator, SURVEY 8d)",
-        "config": {"workload": f"config{args.config}: {m}x{n} mean-curvature denoise, J={layers}, alpha=0.06",
-                   "sample": f"{cycles} V-cycles per step"},
+        "config": {"workload": desc, "sample": sample},
         "cpu_baseline": {"value": value, "unit": "Mpixel-sweeps/s", "cores": threads, "kind": "port",
-                         "sample": f"{cycles} V-cycles of config {args.config} per step (oracle/cmg_oracle.c, "
-                                   f"OpenMP over patches, {threads} threads)"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": "Mpixel-sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args):
-    import ctypes
+class Pinned:
+    """Pinned host array (cmg_host_alloc) for the end-to-end leg."""
 
+    def __init__(self, shape, dtype):
+        from paper_2204_07921_b200 import _native as N
+
+        self.N = N
+        self.nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        self.p = N.lib().cmg_host_alloc(self.nbytes)
+        self.a = np.frombuffer((ctypes.c_char * self.nbytes).from_address(self.p), dtype=dtype).reshape(shape)
+
+    def free(self):
+        self.N.lib().cmg_host_free(self.p)
+
+
+def run_ours(args):
     import torch
 
     ws, rank, local = dist_env()
     if ws > 1:
         import torch.distributed as dist
 
+        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     from paper_2204_07921_b200 import _native as N
     from paper_2204_07921_b200 import synth
 
-    c = synth.CONFIGS[args.config]
-    f, clean = synth.config_input(args.config, 0, fp32=(args.dtype == "float32"))
-    m, n = f.shape
-    layers = c["layers"]
-    eps = c.get("eps", 1e-300)
+    c, size, layers, eps, batch, desc = workload(args.config, args.dtype, args.precision)
     max_outer = c["cycles"]
-    prec = args.precision
-    plan = N.Plan(m, n, 1, layers, c["mode"], args.dtype, prec, device=local)
-    L = N.lib()
     dt = np.float64 if args.dtype == "float64" else np.float32
     esz = np.dtype(dt).itemsize
-    nbytes = m * n * esz
-    # pinned host buffers for the end-to-end leg
-    hp_f = L.cmg_host_alloc(nbytes)
-    hp_u = L.cmg_host_alloc(nbytes)
-    f_h = np.frombuffer((ctypes.c_char * nbytes).from_address(hp_f), dtype=dt).reshape(m, n)
-    u_h = np.frombuffer((ctypes.c_char * nbytes).from_address(hp_u), dtype=dt).reshape(m, n)
-    f_h[...] = f.astype(dt)
-    cap = max_outer + 1
-    en = np.zeros(cap)
-    its = np.zeros(1, dtype=np.int32)
-    sts = np.zeros(1, dtype=np.int32)
-
-    def solve_host():
-        rc = L.cmg_solve(plan.handle, N.ptr(f_h), None, N.ptr(u_h), 0.06, eps, max_outer, 1, 0, 0, 1.0,
-                         N.dptr(en), None, None, None, None, N.iptr(its), N.iptr(sts))
-        assert rc in (0, 2), N.last_error()
-
-    def solve_dev():
-        rc = L.cmg_solve_device(plan.handle, None, None, None, 0.06, eps, max_outer, 1, 0, 0, 1.0,
-                                N.dptr(en), None, None, None, None, N.iptr(its), N.iptr(sts))
-        assert rc in (0, 2), N.last_error()
-
+    L = N.lib()
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
     def l2_flush():
         flush.random_(0, 255)
         torch.cuda.synchronize()
 
-    solve_host()  # uploads f and builds the graph
-    for _ in range(max(args.warmup, 3)):
-        solve_dev()
-    cycles = int(its[0])
-    # ---- device-resident timed region (CUDA events inside libcmg around each solve) ----
-    sampler = ClockSampler(local)
-    sampler.start()
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    dev_ms = []
-    launches = 0
-    for _ in range(args.steps):
-        l2_flush()
-        solve_dev()
-        st = plan.stats()
-        dev_ms.append(st["device_ms"])
-        launches += st["kernel_launches"]
-    torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-    clocks = sampler.stop()
-    ms_step = float(np.mean(dev_ms))
-    # ---- end-to-end through the C ABI with pinned host buffers ----
-    e2e_t = []
-    for _ in range(args.steps):
-        l2_flush()
-        t0 = time.perf_counter()
-        solve_host()
-        e2e_t.append(time.perf_counter() - t0)
-    e2e_ms = 1e3 * float(np.mean(e2e_t))
-    # ---- roofline: level-1 four-colour sweep, CUDA events on the plan's stream ----
-    l1_ms = plan.time_sweep(1, -1, reps=50)
-    lvl_ms = {j: plan.time_sweep(j, -1, reps=20) for j in range(2, layers + 1)}
-    px_sweeps = cycles * layers * m * n
-    if ws > 1:
-        tt = torch.tensor([ms_step, e2e_ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms_step, e2e_ms = float(tt[0]), float(tt[1])
-    value = ws * px_sweeps / (ms_step * 1e-3) / 1e6
-    e2e_value = ws * px_sweeps / (e2e_ms * 1e-3) / 1e6
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(*vals):
+        if ws == 1:
+            return vals
+        t = torch.tensor(vals, device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return tuple(float(x) for x in t)
+
+    extra = {}
+    if args.config == 5 and ws > 1:
+        value_ms, e2e_ms, cycles, launches, clocks, nbytes_in, nbytes_out, l1_ms, m_loc = run_strips(
+            args, c, layers, dt, ws, rank, local, l2_flush, barrier, max_over_ranks)
+        m, n = size, size
+        px_sweeps = cycles * layers * m * n
+        imgs_total = 1
+        parallelism = f"strips x{ws} (NCCL ghost rows after every level)"
+        plan = None
+    else:
+        # images handled by this rank
+        if args.config == 4:
+            per = batch // ws
+            idx = list(range(rank * per, (rank + 1) * per))
+            parallelism = f"dp{ws} (images sharded, no collective)" if ws > 1 else "single GPU, batch 64"
+        else:
+            idx = [0]
+            parallelism = f"replicas x{ws}" if ws > 1 else "single GPU"
+        fs = np.stack([synth.config_input(args.config, i, fp32=(args.dtype == "float32"))[0] for i in idx])
+        B, m, n = fs.shape
+        plan = N.Plan(m, n, B, layers, c["mode"], args.dtype, args.precision, device=local)
+        nbytes = B * m * n * esz
+        f_h = Pinned((B, m, n), dt)
+        u_h = Pinned((B, m, n), dt)
+        f_h.a[...] = fs.astype(dt)
+        cap = max_outer + 1
+        en = np.zeros(B * cap)
+        its = np.zeros(B, dtype=np.int32)
+        sts = np.zeros(B, dtype=np.int32)
+
+        def solve_host():
+            rc = L.cmg_solve(plan.handle, N.ptr(f_h.a), None, N.ptr(u_h.a), 0.06, eps, max_outer, 1, 0, 0, 1.0,
+                             N.dptr(en), None, None, None, None, N.iptr(its), N.iptr(sts))
+            assert rc in (0, 2), N.last_error()
+
+        def solve_dev():
+            rc = L.cmg_solve_device(plan.handle, None, None, None, 0.06, eps, max_outer, 1, 0, 0, 1.0,
+                                    N.dptr(en), None, None, None, None, N.iptr(its), N.iptr(sts))
+            assert rc in (0, 2), N.last_error()
+
+        solve_host()  # uploads f, builds the graph
+        for _ in range(max(args.warmup, 3)):
+            solve_dev()
+        cycles = int(its.max())
+        sampler = ClockSampler(local)
+        sampler.start()
+        barrier()
+        dev_ms, launches = [], 0
+        for _ in range(args.steps):
+            l2_flush()
+            solve_dev()  # CUDA events on the plan's stream bracket the whole solve
+            st = plan.stats()
+            dev_ms.append(st["device_ms"])
+            launches += st["kernel_launches"]
+        barrier()
+        clocks = sampler.stop()
+        e2e_t = []
+        for _ in range(args.steps):
+            l2_flush()
+            barrier()
+            t0 = time.perf_counter()
+            solve_host()  # H2D of f from pinned memory, solve, D2H of u + trace
+            e2e_t.append(time.perf_counter() - t0)
+        value_ms = float(np.mean(dev_ms))
+        e2e_ms = 1e3 * float(np.mean(e2e_t))
+        value_ms, e2e_ms = max_over_ranks(value_ms, e2e_ms)
+        l1_ms = plan.time_sweep(1, -1, reps=50)
+        extra["level_sweep_ms"] = {"1": l1_ms, **{str(j): plan.time_sweep(j, -1, reps=20)
+                                                  for j in range(2, layers + 1)}}
+        px_sweeps = cycles * layers * m * n * B * ws
+        imgs_total = B * ws
+        nbytes_in, nbytes_out = nbytes, nbytes + 8 * cap * B
+        m_loc = m
+        f_h.free()
+        u_h.free()
+    value = px_sweeps / (value_ms * 1e-3) / 1e6
+    e2e_value = px_sweeps / (e2e_ms * 1e-3) / 1e6
     peak, peak_src = measured_peaks()
-    alg_bytes = 3 * esz * m * n  # read u, read f, write u per pixel-sweep
+    # dominant kernel: the level-1 sweep (fused four-colour tile kernel);
+    # algorithmic bytes = 3*sizeof(T) per pixel (read u, read f, write u, SURVEY 8d)
+    alg_bytes = 3 * esz * m_loc * n * (1 if args.config != 4 else len(idx))
     achieved = alg_bytes / (l1_ms * 1e-3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get(f"config{args.config}_{args.dtype}_{args.precision}_l1")
+        except Exception:
+            traffic = None
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         from oracle import oracle as O
 
         thr = O.max_threads()
-        v, dtc, _ = cpu_sample(f, layers, args.ref_cycles, thr)
+        fc, _ = synth.config_input(args.config, 0, fp32=(args.dtype == "float32"))
+        if args.config == 5:
+            fc = fc[:2048]
+        v, dtc = cpu_sample(fc, layers, args.ref_cycles, thr, c["mode"])
         cpu = {"value": v, "unit": "Mpixel-sweeps/s", "cores": thr, "kind": "port",
-               "sample": f"{args.ref_cycles} V-cycles of config {args.config} ({dtc:.1f} s, oracle/cmg_oracle.c, "
-                         f"OpenMP {thr} threads)"}
-    traffic = None
-    tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
-        try:
-            traffic = json.loads(tp.read_text()).get(f"{args.dtype}_{prec}_l1")
-        except Exception:
-            traffic = None
+               "sample": f"{args.ref_cycles} V-cycles of {fc.shape[0]}x{fc.shape[1]} (config {args.config}) in "
+                         f"{dtc:.1f} s; oracle/cmg_oracle.c, OpenMP {thr} threads"}
     line = {
-        "metric": "Mpixel-sweeps/s (1024^2 MC denoise to tolerance, J=3)",
+        "metric": "Mpixel-sweeps/s",
         "value": value,
         "unit": "Mpixel-sweeps/s",
         "n_gpus": ws,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": ms_step,
+        "ms_per_step": value_ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if args.config != 5 else "strong",
         "vs_baseline": None,
         "dtype": "f64" if args.dtype == "float64" else "f32",
         "data": "synthetic (BASELINE seeded generator, SURVEY 8d)",
-        "config": {"workload": f"config{args.config}: {m}x{n} mean-curvature denoise, J={layers}, alpha=0.06, "
-                               f"eps={eps:g}, precision={prec}",
-                   "cycles_to_tolerance": cycles, "time_to_tolerance_ms": ms_step,
-                   "l2": "flushed (512 MiB write) before every timed step; working set is L2-resident within a solve",
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                   "level_sweep_ms": {"1": l1_ms, **{str(k): v for k, v in lvl_ms.items()}}},
-        "e2e": {"value": e2e_value, "unit": "Mpixel-sweeps/s", "h2d_bytes_per_step": nbytes,
-                "d2h_bytes_per_step": nbytes + 8 * cap, "ms_per_step": e2e_ms},
+        "config": {"workload": desc, "images": imgs_total, "cycles": cycles, "time_to_tolerance_ms": value_ms,
+                   "l2": "flushed (512 MiB write) before every timed step; a 1024^2 solve is L2-resident after "
+                         "its first sweep",
+                   "parallelism": parallelism, **extra},
+        "e2e": {"value": e2e_value, "unit": "Mpixel-sweeps/s", "h2d_bytes_per_step": int(nbytes_in),
+                "d2h_bytes_per_step": int(nbytes_out), "ms_per_step": e2e_ms,
+                "path": "cmg_solve (C ABI) with pinned host buffers"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_sweep_tpp level 1 (4 colour launches)",
-                     "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+                     "traffic": traffic, "kernel": "k_level_fused<level 1> (all four colours in one launch)",
+                     "algorithmic_bytes_per_launch": int(alg_bytes), "launch_ms": l1_ms, "peak_source": peak_src},
         "clocks": clocks,
     }
     if cpu:
         line["cpu_baseline"] = cpu
     if rank == 0:
         print(json.dumps(line), flush=True)
-    L.cmg_host_free(hp_f)
-    L.cmg_host_free(hp_u)
-    plan.close()
+    if plan is not None:
+        plan.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_strips(args, c, layers, dt, ws, rank, local, l2_flush, barrier, max_over_ranks):
+    """config 5: one image, horizontal strips (one per rank)."""
+    import torch
+
+    from paper_2204_07921_b200 import strips as S
+    from paper_2204_07921_b200 import synth
+    from paper_2204_07921_b200.driver import SolverConfig
+
+    f, _ = synth.config_input(5, 0, fp32=True)
+    m, n = f.shape
+    cfg = SolverConfig(mode="mean", layers=layers, max_outer=c["cycles"], epsilon=1e-300, dtype=args.dtype,
+                       precision=args.precision, device=local)
+    G = S.ghost_rows(layers)
+    geoms = [S.StripGeometry(m, n, g0, g1, G) for g0, g1 in S.partition_rows(m, ws, layers)]
+    g = geoms[rank]
+    st = S.CudaStrip(g, cfg, local)
+    win = np.ascontiguousarray(f[g.w0:g.w1].astype(dt))
+    st.upload(3, win)
+    if ws > 1:
+        ex = S.DistExchange(st, geoms, rank)
+    else:
+        ex = S.LocalExchange([st])
+
+    def solve():
+        st.upload(0, win)
+        return S.solve_strips([st], ex, cfg, m * n)
+
+    for _ in range(max(args.warmup, 3)):
+        solve()
+    sampler = ClockSampler(local)
+    sampler.start()
+    times = []
+    cycles = 0
+    for _ in range(args.steps):
+        l2_flush()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, tr = solve()
+        e1.record()
+        barrier()
+        times.append(e0.elapsed_time(e1))
+        cycles = tr.iterations
+    clocks = sampler.stop()
+    ms = float(np.mean(times))
+    e2e = []
+    for _ in range(args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        st.upload(0, win)
+        cur, tr = S.solve_strips([st], ex, cfg, m * n)
+        own = st.download(cur)[g.local(g.g0):g.local(g.g1)]
+        barrier()
+        e2e.append(time.perf_counter() - t0)
+    e2e_ms = 1e3 * float(np.mean(e2e))
+    ms, e2e_ms = max_over_ranks(ms, e2e_ms)
+    l1_ms = st.plan.time_sweep(1, -1, reps=5)
+    esz = np.dtype(dt).itemsize
+    st.close()
+    launches = cycles * (layers + 1) + 1
+    return (ms, e2e_ms, cycles, launches, clocks, win.nbytes * ws, own.nbytes * ws, l1_ms, g.rows)
 
 
 def main():
@@ -313,12 +433,16 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--dtype", choices=["float64", "float32"], default="float64")
-    ap.add_argument("--precision", choices=["exact", "fast"], default="exact")
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--dtype", choices=["float64", "float32"], default=None)
+    ap.add_argument("--precision", choices=["exact", "fast"], default=None)
     ap.add_argument("--ref-cycles", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.dtype is None:
+        args.dtype = "float32" if args.config in (4, 5) else "float64"
+    if args.precision is None:
+        args.precision = "fast" if args.dtype == "float32" else "exact"
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -119,6 +119,25 @@ int cmg_plan_stats(cmg_plan* plan, long long* kernel_launches, int* cycles_run, 
  */
 int cmg_time_sweep(cmg_plan* plan, int layer, int color, int reps, double* ms_per_launch);
 
+/*
+ * Building blocks for host-driven decompositions (horizontal strips over
+ * several GPUs, paper_2204_07921_b200/strips.py).  A plan owns five device
+ * buffers: 0..2 = the u rotation buffers, 3 = f, 4 = reference image.
+ */
+/* device pointer of buffer `index` (batch*m*n elements) */
+int cmg_plan_buffer(cmg_plan* plan, int index, void** dev_ptr);
+/* whole-buffer host->device / device->host copies */
+int cmg_buffer_upload(cmg_plan* plan, int index, const void* host);
+int cmg_buffer_download(cmg_plan* plan, int index, void* host);
+/* one level visit (driver.sweep_layer, driver.py:225-251) reading buffer
+ * in_index and writing buffer out_index (distinct, 0..2) */
+int cmg_level_step(cmg_plan* plan, int layer, int in_index, int out_index, double alpha, int inner_iters);
+/* raw energy sums over rows [row_lo,row_hi) of every image: out[batch][5] =
+ * {sum curvature (tangent.py:313-325), sum (u-f)^2, sum |u-u_prev|, sum |u|,
+ *  sum (u-ref)^2}; F = s0 + (alpha/2) s1 as in tangent.energy (tangent.py:339-341) */
+int cmg_energy_partials(cmg_plan* plan, int u_index, int prev_index, int use_ref, int row_lo, int row_hi,
+                        double* out);
+
 /* Pinned host memory helpers (for host<->device copies at full PCIe rate). */
 void* cmg_host_alloc(unsigned long long bytes);
 int cmg_host_free(void* p);

@@ -23,7 +23,8 @@ STOP = {"rel_energy": 0, "rel_u": 1}
 SYMBOLS = (
     "cmg_version", "cmg_last_error", "cmg_device_count", "cmg_plan_create", "cmg_plan_destroy", "cmg_solve",
     "cmg_solve_device", "cmg_sweep_layer", "cmg_energy", "cmg_plane_table", "cmg_plan_stats", "cmg_time_sweep",
-    "cmg_host_alloc", "cmg_host_free",
+    "cmg_host_alloc", "cmg_host_free", "cmg_plan_buffer", "cmg_buffer_upload", "cmg_buffer_download",
+    "cmg_level_step", "cmg_energy_partials",
 )
 
 
@@ -70,6 +71,16 @@ def _declare(L):
     L.cmg_host_alloc.argtypes = [ctypes.c_ulonglong]
     L.cmg_host_free.restype = _i
     L.cmg_host_free.argtypes = [_vp]
+    L.cmg_plan_buffer.restype = _i
+    L.cmg_plan_buffer.argtypes = [_vp, _i, ctypes.POINTER(_vp)]
+    L.cmg_buffer_upload.restype = _i
+    L.cmg_buffer_upload.argtypes = [_vp, _i, _vp]
+    L.cmg_buffer_download.restype = _i
+    L.cmg_buffer_download.argtypes = [_vp, _i, _vp]
+    L.cmg_level_step.restype = _i
+    L.cmg_level_step.argtypes = [_vp, _i, _i, _i, _d, _i]
+    L.cmg_energy_partials.restype = _i
+    L.cmg_energy_partials.argtypes = [_vp, _i, _i, _i, _i, _i, _dp]
 
 
 def lib():

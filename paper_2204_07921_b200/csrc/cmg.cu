@@ -224,10 +224,10 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
         if (!P->fused) CK(cudaMemcpyAsync(P->uprev, P->f, bytes, cudaMemcpyDeviceToDevice, P->stream));
         if (P->dtype == CMG_F64) {
             enqueue_fpads<double>(P);
-            enqueue_energy_ptrs<double>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1);
+            enqueue_energy_ptrs<double>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1, nullptr, 0, -1);
         } else {
             enqueue_fpads<float>(P);
-            enqueue_energy_ptrs<float>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1);
+            enqueue_energy_ptrs<float>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1, nullptr, 0, -1);
         }
         CK(cudaGetLastError());
         const int init_launches = P->enq;
@@ -317,7 +317,7 @@ int cmg_plan_destroy(cmg_plan* P) {
     cudaSetDevice(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     if (P->exec) cudaGraphExecDestroy(P->exec);
-    void* ptrs[] = {P->u, P->uprev, P->ubuf[2], P->f, P->ref, P->upad, P->epad, P->partials, P->st, P->ndone, P->eonly, P->P};
+    void* ptrs[] = {P->u, P->uprev, P->ubuf[2], P->f, P->ref, P->upad, P->epad, P->partials, P->st, P->ndone, P->eonly, P->raw5, P->P};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 5; ++i)
@@ -427,6 +427,7 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     CKP(cudaMalloc(&P->ndone, sizeof(int) * 2));
     P->iters = P->ndone + 1;
     CKP(cudaMalloc(&P->eonly, sizeof(double) * batch));
+    CKP(cudaMalloc(&P->raw5, sizeof(double) * NSUM * batch));
     CKP(cudaMalloc(&P->P, sizeof(SolveParams)));
 #undef CKP
     *out = P;
@@ -531,9 +532,9 @@ int cmg_energy(cmg_plan* P, const void* u_host, const void* f_host, double alpha
     CK(cudaMemcpyAsync(P->uprev, u_host, bytes, cudaMemcpyHostToDevice, P->stream));
     CK(cudaMemcpyAsync(P->f, f_host, bytes, cudaMemcpyHostToDevice, P->stream));
     if (P->dtype == CMG_F64)
-        enqueue_energy<double>(P, false, P->eonly, 0);
+        enqueue_energy_ptrs<double>(P, P->u, P->uprev, false, P->eonly, 0, nullptr, 0, -1);
     else
-        enqueue_energy<float>(P, false, P->eonly, 0);
+        enqueue_energy_ptrs<float>(P, P->u, P->uprev, false, P->eonly, 0, nullptr, 0, -1);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(energy_out, P->eonly, sizeof(double) * P->B, cudaMemcpyDeviceToHost, P->stream));
     CK(cudaStreamSynchronize(P->stream));
@@ -589,6 +590,115 @@ int cmg_time_sweep(cmg_plan* P, int layer, int color, int reps, double* ms_per_l
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, P->e0, P->e1));
     *ms_per_launch = (double)ms / reps;
+    return CMG_OK;
+}
+
+static void* buffer_ptr(cmg_plan* P, int index) {
+    if (index >= 0 && index <= 2) return P->ubuf[index];
+    if (index == 3) return P->f;
+    if (index == 4) {
+        if (!P->ref) cudaMalloc(&P->ref, P->esz * (size_t)P->N * P->B);
+        return P->ref;
+    }
+    return nullptr;
+}
+
+int cmg_plan_buffer(cmg_plan* P, int index, void** dev_ptr) {
+    if (!P || !dev_ptr) return fail(CMG_EINVAL, "NULL argument");
+    int rc = set_device(P);
+    if (rc) return rc;
+    void* p = buffer_ptr(P, index);
+    if (!p) return fail(CMG_EINVAL, "buffer index must be 0..4");
+    *dev_ptr = p;
+    return CMG_OK;
+}
+
+int cmg_buffer_upload(cmg_plan* P, int index, const void* host) {
+    if (!P || !host) return fail(CMG_EINVAL, "NULL argument");
+    int rc = set_device(P);
+    if (rc) return rc;
+    void* p = buffer_ptr(P, index);
+    if (!p) return fail(CMG_EINVAL, "buffer index must be 0..4");
+    CK(cudaMemcpyAsync(p, host, P->esz * (size_t)P->N * P->B, cudaMemcpyHostToDevice, P->stream));
+    if (index == 3) {  // f changed: refresh the padded f of general levels
+        if (P->dtype == CMG_F64)
+            enqueue_fpads<double>(P);
+        else
+            enqueue_fpads<float>(P);
+    }
+    CK(cudaStreamSynchronize(P->stream));
+    return CMG_OK;
+}
+
+int cmg_buffer_download(cmg_plan* P, int index, void* host) {
+    if (!P || !host) return fail(CMG_EINVAL, "NULL argument");
+    int rc = set_device(P);
+    if (rc) return rc;
+    void* p = buffer_ptr(P, index);
+    if (!p) return fail(CMG_EINVAL, "buffer index must be 0..4");
+    CK(cudaMemcpyAsync(host, p, P->esz * (size_t)P->N * P->B, cudaMemcpyDeviceToHost, P->stream));
+    CK(cudaStreamSynchronize(P->stream));
+    return CMG_OK;
+}
+
+int cmg_level_step(cmg_plan* P, int layer, int in_index, int out_index, double alpha, int inner_iters) {
+    if (!P) return fail(CMG_EINVAL, "plan is NULL");
+    if (layer < 1 || layer > P->layers) return fail(CMG_EINVAL, "layer outside the plan's hierarchy");
+    if (in_index < 0 || in_index > 2 || out_index < 0 || out_index > 2 || in_index == out_index)
+        return fail(CMG_EINVAL, "in/out must be distinct rotation buffers 0..2");
+    int rc = check_cfg(alpha, 1.0, 1, inner_iters, 0);
+    if (rc) return rc;
+    rc = set_device(P);
+    if (rc) return rc;
+    SolveParams sp;
+    fill_params(P, sp, alpha, 1.0, 1, inner_iters, 0, false, 1.0);
+    CK(cudaMemcpyAsync(P->P, &sp, sizeof(sp), cudaMemcpyHostToDevice, P->stream));
+    CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
+    const bool fusedj = P->fused && layer <= 3 && ((P->fuse_mask >> (layer - 1)) & 1);
+    if (fusedj) {
+        if (P->dtype == CMG_F64)
+            enqueue_fused_level<double>(P, layer, P->ubuf[in_index], P->ubuf[out_index]);
+        else
+            enqueue_fused_level<float>(P, layer, P->ubuf[in_index], P->ubuf[out_index]);
+    } else {
+        CK(cudaMemcpyAsync(P->ubuf[out_index], P->ubuf[in_index], P->esz * (size_t)P->N * P->B,
+                           cudaMemcpyDeviceToDevice, P->stream));
+        void* save = P->u;
+        P->u = P->ubuf[out_index];
+        for (int c = 0; c < 4; ++c) {
+            if (P->dtype == CMG_F64)
+                enqueue_sweep<double>(P, layer, c);
+            else
+                enqueue_sweep<float>(P, layer, c);
+        }
+        P->u = save;
+    }
+    CK(cudaGetLastError());
+    std::vector<ImgState> hs(P->B);
+    CK(cudaMemcpyAsync(hs.data(), P->st, sizeof(ImgState) * P->B, cudaMemcpyDeviceToHost, P->stream));
+    CK(cudaStreamSynchronize(P->stream));
+    for (int b = 0; b < P->B; ++b)
+        if (hs[b].bad) return fail(CMG_ENONFINITE, "corrections must be finite");
+    return CMG_OK;
+}
+
+int cmg_energy_partials(cmg_plan* P, int u_index, int prev_index, int use_ref, int row_lo, int row_hi,
+                        double* out) {
+    if (!P || !out) return fail(CMG_EINVAL, "NULL argument");
+    if (u_index < 0 || u_index > 2 || prev_index < 0 || prev_index > 2) return fail(CMG_EINVAL, "bad buffer index");
+    if (row_lo < 0 || row_hi > P->m || row_lo > row_hi) return fail(CMG_EINVAL, "bad row range");
+    int rc = set_device(P);
+    if (rc) return rc;
+    if (use_ref && !P->ref) return fail(CMG_EINVAL, "no reference uploaded (buffer 4)");
+    CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
+    const long long lo = (long long)row_lo * P->n, hi = (long long)row_hi * P->n;
+    if (P->dtype == CMG_F64)
+        enqueue_energy_ptrs<double>(P, P->ubuf[u_index], P->ubuf[prev_index], use_ref != 0, nullptr, 0, P->raw5, lo, hi);
+    else
+        enqueue_energy_ptrs<float>(P, P->ubuf[u_index], P->ubuf[prev_index], use_ref != 0, nullptr, 0, P->raw5, lo, hi);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, P->raw5, sizeof(double) * NSUM * P->B, cudaMemcpyDeviceToHost, P->stream));
+    CK(cudaStreamSynchronize(P->stream));
     return CMG_OK;
 }
 

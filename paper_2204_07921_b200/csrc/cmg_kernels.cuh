@@ -527,7 +527,8 @@ struct EnergyArgs {
     const void* upad;  // padded (pad 1) snapshot when SRC_PADDED
     long long istride, pstride;
     int m, n, W, mode, nbx;
-    double* partials;  // [B][nbx][5]
+    long long e_lo, e_hi;  // pixel index range of the sums (whole image: 0..m*n)
+    double* partials;      // [B][nbx][5]
     const ImgState* st;
 };
 
@@ -542,8 +543,7 @@ __global__ void __launch_bounds__(256) k_energy(EnergyArgs a) {
         const T* f = (const T*)a.f + (long long)b * a.istride;
         const T* up = (const T*)a.uprev + (long long)b * a.istride;
         const T* rf = a.ref ? (const T*)a.ref + (long long)b * a.istride : nullptr;
-        const long long N = (long long)a.m * a.n;
-        for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < N;
+        for (long long e = a.e_lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; e < a.e_hi;
              e += (long long)a.nbx * blockDim.x) {
             const int i = (int)(e / a.n), k = (int)(e % a.n);
             double uo, uE, uW, uN, uS, uNE, uSW, uNW, uSE;
@@ -619,6 +619,7 @@ struct TraceArgs {
     int cap;
     int* ndone;
     double* eonly;  // energy-only mode output [B] (nullptr in solve)
+    double* raw5;   // raw partial sums [B][5] (strip mode), or nullptr
 };
 
 // One CTA per image: reduce partials in a fixed order, record the trace and
@@ -627,7 +628,7 @@ static __global__ void __launch_bounds__(256) k_finalize(const double* partials,
                                                   ImgState* st, TraceArgs tr, int initial) {
     const int b = blockIdx.x;
     ImgState& S = st[b];
-    if (!initial && tr.eonly == nullptr && S.done) return;
+    if (!initial && tr.eonly == nullptr && tr.raw5 == nullptr && S.done) return;
     __shared__ double sh[NSUM][256];
     double acc[NSUM] = {0, 0, 0, 0, 0};
     for (int i = threadIdx.x; i < nbx; i += blockDim.x)
@@ -644,6 +645,10 @@ static __global__ void __launch_bounds__(256) k_finalize(const double* partials,
     }
     if (threadIdx.x != 0) return;
     const double curv = sh[0][0], fid = sh[1][0], du = sh[2][0], au = sh[3][0], dr = sh[4][0];
+    if (tr.raw5) {
+        for (int s = 0; s < NSUM; ++s) tr.raw5[b * NSUM + s] = sh[s][0];
+        return;
+    }
     const double F = curv + P->half_alpha * fid;
     if (tr.eonly) {
         tr.eonly[b] = F;

@@ -141,7 +141,8 @@ void enqueue_copy_prev(cmg_plan* P) {
 }
 
 template <typename T>
-void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has_ref, double* eonly, int initial) {
+void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has_ref, double* eonly, int initial,
+                         double* raw5, long long e_lo, long long e_hi) {
     if (P->egeneral) enqueue_pad<T>(P, u, P->epad, P->eH, P->eW, P->epstride, 1, 1, !initial && !eonly);
     EnergyArgs ea;
     ea.u = u;
@@ -156,6 +157,8 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
     ea.W = P->eW;
     ea.mode = P->mode;
     ea.nbx = P->nbx;
+    ea.e_lo = e_lo;
+    ea.e_hi = e_hi < 0 ? P->N : e_hi;
     ea.partials = P->partials;
     ea.st = P->st;
     if (P->egeneral)
@@ -171,13 +174,14 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
     ta.cap = P->cap;
     ta.ndone = P->ndone;
     ta.eonly = eonly;
+    ta.raw5 = raw5;
     k_finalize<<<P->B, 256, 0, P->stream>>>(P->partials, P->nbx, P->P, P->st, ta, initial);
     P->enq += 2;
 }
 
 template <typename T>
 void enqueue_energy(cmg_plan* P, bool has_ref, double* eonly, int initial) {
-    enqueue_energy_ptrs<T>(P, P->u, P->uprev, has_ref, eonly, initial);
+    enqueue_energy_ptrs<T>(P, P->u, P->uprev, has_ref, eonly, initial, nullptr, 0, -1);
 }
 
 // tile sizes (patches per tile side) and lanes per patch of the fused levels
@@ -290,7 +294,7 @@ void enqueue_body_fused(cmg_plan* P, int full, bool has_ref) {
                 P->u = save;
             }
         }
-        enqueue_energy_ptrs<T>(P, P->ubuf[cur], P->ubuf[prev], has_ref, nullptr, 0);
+        enqueue_energy_ptrs<T>(P, P->ubuf[cur], P->ubuf[prev], has_ref, nullptr, 0, nullptr, 0, -1);
     }
 }
 
@@ -339,6 +343,7 @@ cudaError_t persist_launch_v(cmg_plan* P, bool has_ref, int full) {
     a.tr.cap = P->cap;
     a.tr.ndone = P->ndone;
     a.tr.eonly = nullptr;
+    a.tr.raw5 = nullptr;
     const size_t smem = sizeof(double) * P->B + sizeof(int) * ((P->B + 1) & ~1) + sizeof(double) * NSUM * 32 +
                         sizeof(T) * (64 + 256 + 2);
     cudaError_t e;
@@ -384,5 +389,6 @@ cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full) {
     template void cmg::enqueue_fpads<T>(cmg_plan*);                             \
     template cudaError_t cmg::persist_launch<T>(cmg_plan*, bool, int);               \
     template void cmg::enqueue_fused_level<T>(cmg_plan*, int, const void*, void*);  \
-    template void cmg::enqueue_energy_ptrs<T>(cmg_plan*, const void*, const void*, bool, double*, int); \
+    template void cmg::enqueue_energy_ptrs<T>(cmg_plan*, const void*, const void*, bool, double*, int, double*, \
+                                              long long, long long);                                   \
     template void cmg::enqueue_body_fused<T>(cmg_plan*, int, bool);

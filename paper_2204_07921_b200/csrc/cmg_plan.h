@@ -37,6 +37,7 @@ struct cmg_plan {
     int* ndone = nullptr;
     int* iters = nullptr;
     double* eonly = nullptr;
+    double* raw5 = nullptr;  // [B][5] strip-mode partial sums
     cmg::SolveParams* P = nullptr;
     double* tr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     int cap = 0;
@@ -79,7 +80,8 @@ cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full);
 template <typename T>
 void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout);
 template <typename T>
-void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has_ref, double* eonly, int initial);
+void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has_ref, double* eonly, int initial,
+                         double* raw5, long long e_lo, long long e_hi);
 template <typename T>
 void enqueue_body_fused(cmg_plan* P, int full, bool has_ref);
 }  // namespace cmg

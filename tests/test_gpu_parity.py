@@ -183,3 +183,23 @@ def test_launch_stats_reported():
     st = get_plan(256, 256, 1, cfg).stats()
     # fused levels: >= J fused launches + energy + finalize per cycle (or 1 persistent launch)
     assert st["cycles_run"] == 4 and st["kernel_launches"] >= 1
+
+
+@pytest.mark.parametrize("parts,mode,dtype", [(2, "mean", "float64"), (3, "gaussian", "float64"),
+                                              (4, "mean", "float32")])
+def test_virtual_strips_equal_single_gpu_solve(parts, mode, dtype):
+    """Strip decomposition on one GPU (virtual strips, D2D ghost exchange) ==
+    the single-plan solve, bit for bit."""
+    from paper_2204_07921_b200.strips import denoise_strips
+
+    f, cl = synth.config_input(1)
+    f = f[:, :200]
+    cl = cl[:, :200]
+    cfg = cmg.SolverConfig(mode=mode, layers=3, max_outer=6, epsilon=1e-300, dtype=dtype,
+                           precision="fast" if dtype == "float32" else "exact")
+    u1, t1 = cmg.denoise(cmg.Image(f, 1.0), cfg, cmg.Image(cl, 1.0))
+    u2, t2 = denoise_strips(cmg.Image(f, 1.0), cfg, parts=parts, reference=cmg.Image(cl, 1.0))
+    assert np.array_equal(u1.data, u2.data)
+    assert t1.iterations == t2.iterations
+    rtol = 1e-12 if dtype == "float64" else 1e-9
+    assert np.allclose(t1.energies(), t2.energies(), rtol=rtol, atol=0)
