@@ -360,6 +360,9 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     if (const char* t3 = getenv("CMG_TS3")) P->ts3 = atoi(t3);
     if (const char* fm = getenv("CMG_FUSE_MASK")) P->fuse_mask = atoi(fm) | 1;
     if (const char* dg = getenv("CMG_DBG")) P->dbg = atoi(dg);
+    if (const char* lt = getenv("CMG_L1_TILE")) P->l1_tile = atoi(lt) != 0;
+    if (const char* v2 = getenv("CMG_FCFG2")) P->fcfg2 = atoi(v2);
+    if (const char* v3 = getenv("CMG_FCFG3")) P->fcfg3 = atoi(v3);
     auto bail = [&](int rc) {
         cmg_plan_destroy(P);
         return rc;

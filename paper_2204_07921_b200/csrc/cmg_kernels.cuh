@@ -534,8 +534,26 @@ struct EnergyArgs {
 
 constexpr int NSUM = 5;  // curv, fid, |du|, |u|, (u-ref)^2
 
+// level-1 curvature term of one pixel from its 3x3 neighbourhood, in the
+// accumulation precision A (double for fp64 images, float for fp32 images;
+// the per-row sums are accumulated in double either way)
+template <typename A>
+__device__ __forceinline__ A curv_term(A uo, A uE, A uW, A uN, A uS, A uNE, A uSW, A uNW, A uSE, int mode) {
+    const A two = A(2) * uo;
+    const A k0 = ((uE + uW) - two) * A(0.5);
+    const A k1 = ((uN + uS) - two) * A(0.5);
+    const A k2 = ((uNE + uSW) - two) * A(0.25);
+    const A k3 = ((uNW + uSE) - two) * A(0.25);
+    const A kmin = fmin(fmin(k0, k1), fmin(k2, k3));
+    const A kmax = fmax(fmax(k0, k1), fmax(k2, k3));
+    A term = (mode == MODE_MEAN) ? fabs(A(0.5) * (kmin + kmax)) : fabs(kmin * kmax);
+    if (isnan(k0) || isnan(k1) || isnan(k2) || isnan(k3)) term = A(NAN);
+    return term;
+}
+
 template <typename T, int SRC>
 __global__ void __launch_bounds__(256) k_energy(EnergyArgs a) {
+    using A = T;  // per-pixel precision
     const int b = blockIdx.y;
     double acc[NSUM] = {0, 0, 0, 0, 0};
     if (!a.st[b].done) {
@@ -543,47 +561,50 @@ __global__ void __launch_bounds__(256) k_energy(EnergyArgs a) {
         const T* f = (const T*)a.f + (long long)b * a.istride;
         const T* up = (const T*)a.uprev + (long long)b * a.istride;
         const T* rf = a.ref ? (const T*)a.ref + (long long)b * a.istride : nullptr;
-        for (long long e = a.e_lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; e < a.e_hi;
-             e += (long long)a.nbx * blockDim.x) {
-            const int i = (int)(e / a.n), k = (int)(e % a.n);
-            double uo, uE, uW, uN, uS, uNE, uSW, uNW, uSE;
-            auto ld = [&](const auto& A) {
-                uo = (double)A(i, k);
-                uE = (double)A(i, k + 1);
-                uW = (double)A(i, k - 1);
-                uN = (double)A(i - 1, k);
-                uS = (double)A(i + 1, k);
-                uNE = (double)A(i - 1, k + 1);
-                uSW = (double)A(i + 1, k - 1);
-                uNW = (double)A(i - 1, k - 1);
-                uSE = (double)A(i + 1, k + 1);
-            };
-            if constexpr (SRC == SRC_PADDED) {
-                ld(Padded<T>{(const T*)a.upad + (long long)b * a.pstride, a.W});
-            } else {
-                if (i >= 1 && k >= 1 && i + 1 < a.m && k + 1 < a.n)
-                    ld(Direct<T>{u, a.n});
-                else
-                    ld(Reflect<T>{u, a.m, a.n});
-            }
-            const double two = 2.0 * uo;
-            const double k0 = ((uE + uW) - two) * 0.5;
-            const double k1 = ((uN + uS) - two) * 0.5;
-            const double k2 = ((uNE + uSW) - two) * 0.25;
-            const double k3 = ((uNW + uSE) - two) * 0.25;
-            double kmin = fmin(fmin(k0, k1), fmin(k2, k3));
-            double kmax = fmax(fmax(k0, k1), fmax(k2, k3));
-            double term = (a.mode == MODE_MEAN) ? fabs(0.5 * (kmin + kmax)) : fabs(kmin * kmax);
-            if (isnan(k0) || isnan(k1) || isnan(k2) || isnan(k3)) term = __longlong_as_double(0x7ff8000000000000ULL);
-            const double uv = (double)u[e];
-            const double d = uv - (double)f[e];
-            acc[0] += term;
-            acc[1] += d * d;
-            acc[2] += fabs(uv - (double)up[e]);
-            acc[3] += fabs(uv);
-            if (rf) {
-                const double dr = uv - (double)rf[e];
-                acc[4] += dr * dr;
+        const int n = a.n, m = a.m;
+        const int r_lo = (int)(a.e_lo / n), r_hi = (int)(a.e_hi / n);
+        constexpr int V = 8;  // columns per thread per row (fp32 partial sums of 8 terms)
+        for (int i = r_lo + blockIdx.x; i < r_hi; i += a.nbx) {
+            for (int k0 = threadIdx.x * V; k0 < n; k0 += blockDim.x * V) {
+                A loc[NSUM] = {0, 0, 0, 0, 0};
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) {
+                        A c, E, W, N, S, NE, SW, NW, SE;
+                        auto ld = [&](const auto& U) {
+                            c = (A)U(i, k);
+                            E = (A)U(i, k + 1);
+                            W = (A)U(i, k - 1);
+                            N = (A)U(i - 1, k);
+                            S = (A)U(i + 1, k);
+                            NE = (A)U(i - 1, k + 1);
+                            SW = (A)U(i + 1, k - 1);
+                            NW = (A)U(i - 1, k - 1);
+                            SE = (A)U(i + 1, k + 1);
+                        };
+                        if constexpr (SRC == SRC_PADDED) {
+                            ld(Padded<T>{(const T*)a.upad + (long long)b * a.pstride, a.W});
+                        } else {
+                            if (i >= 1 && k >= 1 && i + 1 < m && k + 1 < n)
+                                ld(Direct<T>{u, n});
+                            else
+                                ld(Reflect<T>{u, m, n});
+                        }
+                        loc[0] += curv_term<A>(c, E, W, N, S, NE, SW, NW, SE, a.mode);
+                        const long long e = (long long)i * n + k;
+                        const A d = c - (A)f[e];
+                        loc[1] += d * d;
+                        loc[2] += fabs(c - (A)up[e]);
+                        loc[3] += fabs(c);
+                        if (rf) {
+                            const A dr = c - (A)rf[e];
+                            loc[4] += dr * dr;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int s = 0; s < NSUM; ++s) acc[s] += (double)loc[s];
             }
         }
     }

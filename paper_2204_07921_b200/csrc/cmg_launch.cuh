@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "cmg_fused.cuh"
+#include "cmg_l1.cuh"
 #include "cmg_persist.cuh"
 #include "cmg_plan.h"
 
@@ -184,25 +185,50 @@ void enqueue_energy(cmg_plan* P, bool has_ref, double* eonly, int initial) {
     enqueue_energy_ptrs<T>(P, P->u, P->uprev, has_ref, eonly, initial, nullptr, 0, -1);
 }
 
-// tile sizes (patches per tile side) and lanes per patch of the fused levels
-template <int LAYER>
+// tile sizes (patches per tile side), lanes per patch and CTA size of the
+// fused levels; variant v selected per plan (CMG_FCFG2 / CMG_FCFG3)
+template <int LAYER, int V>
 struct FusedCfg;
 template <>
-struct FusedCfg<1> {
-    static constexpr int TP = 32, TS = 1;
+struct FusedCfg<1, 0> {
+    static constexpr int TP = 32, TS = 1, NT = 256;
 };
 template <>
-struct FusedCfg<2> {
-    static constexpr int TP = 8, TS = 4;
+struct FusedCfg<2, 0> {
+    static constexpr int TP = 8, TS = 4, NT = 256;
 };
 template <>
-struct FusedCfg<3> {
-    static constexpr int TP = 4, TS = 8;
+struct FusedCfg<2, 1> {
+    static constexpr int TP = 16, TS = 1, NT = 128;
+};
+template <>
+struct FusedCfg<2, 2> {
+    static constexpr int TP = 16, TS = 4, NT = 256;
+};
+template <>
+struct FusedCfg<2, 3> {
+    static constexpr int TP = 32, TS = 1, NT = 256;
+};
+template <>
+struct FusedCfg<3, 0> {
+    static constexpr int TP = 4, TS = 8, NT = 256;
+};
+template <>
+struct FusedCfg<3, 1> {
+    static constexpr int TP = 8, TS = 1, NT = 128;
+};
+template <>
+struct FusedCfg<3, 2> {
+    static constexpr int TP = 8, TS = 8, NT = 256;
+};
+template <>
+struct FusedCfg<3, 3> {
+    static constexpr int TP = 4, TS = 1, NT = 64;
 };
 
-template <typename T, int LAYER, int MODE, int PREC>
-void launch_fused(cmg_plan* P, const FusedArgs<T>& a, int tiles) {
-    constexpr int TP = FusedCfg<LAYER>::TP, TS = FusedCfg<LAYER>::TS;
+template <typename T, int LAYER, int MODE, int PREC, int V>
+void launch_fused(cmg_plan* P, const FusedArgs<T>& a) {
+    constexpr int TP = FusedCfg<LAYER, V>::TP, TS = FusedCfg<LAYER, V>::TS, NT = FusedCfg<LAYER, V>::NT;
     constexpr int RD = FusedGeom<LAYER, TP>::RD;
     const size_t smem = 2 * sizeof(T) * RD * RD;
     auto kern = k_level_fused<T, LAYER, MODE, PREC, TP, TS>;
@@ -211,20 +237,67 @@ void launch_fused(cmg_plan* P, const FusedArgs<T>& a, int tiles) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    kern<<<dim3(tiles, 1, P->B), 256, smem, P->stream>>>(a);
+    const Level& L = P->lv[LAYER];
+    FusedArgs<T> b = a;
+    const int tiles_r = (L.mj + TP - 1) / TP;
+    b.tiles_c = (L.nj + TP - 1) / TP;
+    kern<<<dim3(tiles_r * b.tiles_c, 1, P->B), NT, smem, P->stream>>>(b);
+}
+
+template <typename T>
+struct L1Tile;
+template <>
+struct L1Tile<float> {
+    static constexpr int TH = 32, TW = 64;
+};
+template <>
+struct L1Tile<double> {
+    static constexpr int TH = 32, TW = 32;
+};
+
+template <typename T, int MODE, int PREC>
+void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
+    constexpr int TH = L1Tile<T>::TH, TW = L1Tile<T>::TW;
+    using G = L1Geom<T, TH, TW>;
+    const size_t smem = 2 * sizeof(T) * 4 * G::PLANE;
+    auto kern = k_l1_tile<T, MODE, PREC, TH, TW>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
+    kern<<<grd, 256, smem, P->stream>>>(a);
 }
 
 template <typename T, int MODE, int PREC>
-void dispatch_fused(cmg_plan* P, int layer, const FusedArgs<T>& a, int tiles) {
-    if (layer == 1)
-        launch_fused<T, 1, MODE, PREC>(P, a, tiles);
-    else if (layer == 2)
-        launch_fused<T, 2, MODE, PREC>(P, a, tiles);
-    else
-        launch_fused<T, 3, MODE, PREC>(P, a, tiles);
+void dispatch_fused(cmg_plan* P, int layer, const FusedArgs<T>& a) {
+    if (layer == 1) {
+        if (P->l1_tile)
+            launch_l1_tile<T, MODE, PREC>(P, a);
+        else
+            launch_fused<T, 1, MODE, PREC, 0>(P, a);
+    } else if (layer == 2) {
+        switch (P->fcfg2) {
+            case 1: launch_fused<T, 2, MODE, PREC, 1>(P, a); break;
+            case 2: launch_fused<T, 2, MODE, PREC, 2>(P, a); break;
+            case 3: launch_fused<T, 2, MODE, PREC, 3>(P, a); break;
+            default: launch_fused<T, 2, MODE, PREC, 0>(P, a); break;
+        }
+    } else {
+        switch (P->fcfg3) {
+            case 1: launch_fused<T, 3, MODE, PREC, 1>(P, a); break;
+            case 2:
+                if (sizeof(T) == 4) {
+                    launch_fused<T, 3, MODE, PREC, 2>(P, a);
+                    break;
+                }
+                [[fallthrough]];
+            case 3: launch_fused<T, 3, MODE, PREC, 3>(P, a); break;
+            default: launch_fused<T, 3, MODE, PREC, 0>(P, a); break;
+        }
+    }
 }
-
-inline int fused_tp(int layer) { return layer == 1 ? FusedCfg<1>::TP : layer == 2 ? FusedCfg<2>::TP : FusedCfg<3>::TP; }
 
 template <typename T>
 void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
@@ -238,9 +311,7 @@ void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
     a.n = P->n;
     a.mj = L.mj;
     a.nj = L.nj;
-    const int TP = fused_tp(layer);
-    const int tiles_r = (L.mj + TP - 1) / TP;
-    a.tiles_c = (L.nj + TP - 1) / TP;
+    a.tiles_c = 0;  // set per variant by launch_fused
     for (int c = 0; c < 4; ++c) {
         const int p = c >> 1, q = c & 1;
         a.hc[c] = (L.mj - p + 1) / 2;
@@ -248,13 +319,12 @@ void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
     }
     a.P = P->P;
     a.st = P->st;
-    const int tiles = tiles_r * a.tiles_c;
     if (P->mode == CMG_MODE_GAUSS)
-        dispatch_fused<T, MODE_GAUSS, PREC_EXACT>(P, layer, a, tiles);
+        dispatch_fused<T, MODE_GAUSS, PREC_EXACT>(P, layer, a);
     else if (P->prec == CMG_PREC_FAST)
-        dispatch_fused<T, MODE_MEAN, PREC_FAST>(P, layer, a, tiles);
+        dispatch_fused<T, MODE_MEAN, PREC_FAST>(P, layer, a);
     else
-        dispatch_fused<T, MODE_MEAN, PREC_EXACT>(P, layer, a, tiles);
+        dispatch_fused<T, MODE_MEAN, PREC_EXACT>(P, layer, a);
     P->enq += 1;
 }
 

@@ -43,7 +43,9 @@ struct cmg_plan {
     int cap = 0;
     // kernel variants
     int ts2 = 4, ts3 = 16;
-    int dbg = 0;  // diagnostics bits (CMG_DBG), see SweepArgs::dbg  // team sizes (lanes per patch) of levels 2 and 3
+    int dbg = 0;
+    bool l1_tile = true;
+    int fcfg2 = 0, fcfg3 = 0;  // fused L2/L3 tile variants (FusedCfg)  // dedicated level-1 tile kernel (k_l1_tile) instead of k_level_fused<1>  // diagnostics bits (CMG_DBG), see SweepArgs::dbg  // team sizes (lanes per patch) of levels 2 and 3
     // graphs
     cudaGraphExec_t exec = nullptr;
     int gkey = -1;
