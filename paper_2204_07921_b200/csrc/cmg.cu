@@ -47,6 +47,33 @@ inline bool single_chunk(int len, int pad_after) { return len >= 2 && pad_after 
 
 }  // namespace
 
+namespace cmg {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool make_tmap(CUtensorMap* out, const void* base, int esz, int m, int n, int B, int boxcode) {
+    const int box = boxcode / 4096, boxh = boxcode % 4096;
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return false;
+        fn = (EncodeTiledFn)p;
+    }
+    if (((long long)n * esz) % 16 != 0 || ((long long)box * esz) % 16 != 0 || box > 256 || boxh > 256) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)m, (cuuint64_t)B};
+    const cuuint64_t strides[2] = {(cuuint64_t)n * esz, (cuuint64_t)m * n * esz};
+    const cuuint32_t boxd[3] = {(cuuint32_t)box, (cuuint32_t)boxh, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(out, esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                    const_cast<void*>(base), dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+}  // namespace cmg
+
 namespace {
 
 __global__ void k_cond(cudaGraphConditionalHandle h, const int* ndone, int B, int* iters) {
@@ -361,7 +388,9 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     if (const char* fm = getenv("CMG_FUSE_MASK")) P->fuse_mask = atoi(fm) | 1;
     if (const char* dg = getenv("CMG_DBG")) P->dbg = atoi(dg);
     if (const char* lt = getenv("CMG_L1_TILE")) P->l1_tile = atoi(lt) != 0;
+    if (const char* lx = getenv("CMG_L1X2")) P->l1x2 = atoi(lx);
     if (const char* v2 = getenv("CMG_FCFG2")) P->fcfg2 = atoi(v2);
+    if (const char* ct = getenv("CMG_COARSE_TILE")) P->coarse_tile = atoi(ct) != 0;
     if (const char* v3 = getenv("CMG_FCFG3")) P->fcfg3 = atoi(v3);
     auto bail = [&](int rc) {
         cmg_plan_destroy(P);
@@ -421,6 +450,19 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
         const char* pe = getenv("CMG_PERSIST");
         P->persist = !P->fused && !gen && batch <= 1024 && (pe && pe[0] == '1');
         if (const char* oc = getenv("CMG_OCC")) P->occ_cap = std::max(1, atoi(oc));
+    }
+    {
+        const char* te = getenv("CMG_TMA");
+        const int tmode = te ? atoi(te) : 1;  // 0 off, 1 levels 2-3, 2 / 3 only that level
+        const bool allow = tmode != 0;
+        for (int j = 2; j <= std::min(layers, 3) && allow; ++j) {
+            if (tmode >= 2 && j != tmode) continue;
+            const int box = (dtype == CMG_F64) ? coarse_region<double>(j) : coarse_region<float>(j);
+            bool ok = true;
+            for (int bi = 0; bi < 4 && ok; ++bi)
+                ok = make_tmap(&P->tmap[j][bi], bi < 3 ? P->ubuf[bi] : P->f, (int)P->esz, m, n, batch, box);
+            P->tma_ok[j] = ok;
+        }
     }
     long long want = std::max(1, 1184 / batch);
     P->nbx = (int)std::max(1LL, std::min(want, (P->N + 255) / 256));

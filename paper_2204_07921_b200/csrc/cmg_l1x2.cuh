@@ -1,0 +1,256 @@
+// cmg_l1x2.cuh -- level-1 visit, fp32 fast mean-curvature path, with
+// Blackwell packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2).
+//
+// Same tiling and semantics as k_l1_tile (four colour phases of a TH x TW tile
+// + 4-pixel halo in quad-planar shared memory, u_in -> u_out), but every
+// thread relaxes TWO same-colour pixels of one region row at once: in the
+// quad-planar layout they are adjacent words of one plane, so their
+// neighbourhoods load as 64-bit pairs and the closed-form distance sums
+// run as f32x2 instructions -- half the FP issue slots per
+// pixel.  The reciprocal square roots stay scalar MUFU.RSQ.
+#pragma once
+
+#include "cmg_l1.cuh"
+
+namespace cmg {
+
+struct F2 {
+    unsigned long long v;
+};
+
+__device__ __forceinline__ F2 f2_pack(float lo, float hi) {
+    F2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(F2 a, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+}
+__device__ __forceinline__ F2 f2_splat(float x) { return f2_pack(x, x); }
+__device__ __forceinline__ F2 operator+(F2 a, F2 b) {
+    F2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 operator-(F2 a, F2 b) {
+    F2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 operator*(F2 a, F2 b) {
+    F2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
+// MUFU.RSQ without the subnormal-input fix-up of rsqrtf(): the arguments are
+// S^2 + D^2 + 4|p|^2 >= 4 (never subnormal)
+__device__ __forceinline__ float rsq_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ F2 rsqrt2(F2 a) {
+    F2 r;  // one asm block so the halves stay in their register pair (no moves)
+    asm("{\n\t.reg .f32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\trsqrt.approx.ftz.f32 lo, lo;\n\t"
+        "rsqrt.approx.ftz.f32 hi, hi;\n\tmov.b64 %0, {lo, hi};\n\t}"
+        : "=l"(r.v)
+        : "l"(a.v));
+    return r;
+}
+// reciprocal square root of a pair on the FMA pipe: bit-trick seed + 3 Newton
+// steps in packed fp32 (relative error ~1e-7), used to balance the MUFU pipe
+__device__ __forceinline__ F2 rsqrt2_nr(F2 a) {
+    F2 y;
+    asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\tshr.u32 lo, lo, 1;\n\tshr.u32 hi, hi, 1;\n\t"
+        "sub.u32 lo, 0x5f375a86, lo;\n\tsub.u32 hi, 0x5f375a86, hi;\n\tmov.b64 %0, {lo, hi};\n\t}"
+        : "=l"(y.v)
+        : "l"(a.v));
+    const F2 mh = f2_splat(-0.5f) * a, c15 = f2_splat(1.5f);
+#pragma unroll
+    for (int it = 0; it < 3; ++it) y = y * fma2(mh, y * y, c15);
+    return y;
+}
+__device__ __forceinline__ F2 lds2(const float* p) {
+    F2 r;
+    r.v = *reinterpret_cast<const unsigned long long*>(p);
+    return r;
+}
+
+// closed-form level-1 c_half for two pixels (l1_chalf_fast, packed); NR > 0
+// moves the diagonal pairs' rsqrt to the FMA pipe (balances MUFU)
+template <int NR>
+__device__ __forceinline__ F2 l1_chalf_x2(F2 c, F2 E, F2 W, F2 N, F2 S, F2 NE, F2 NW, F2 SE, F2 SW) {
+    const F2 m2 = f2_splat(-2.f);
+    const F2 four = f2_splat(4.f), eight = f2_splat(8.f);
+    auto pair = [&](F2 up, F2 um, F2 uq, F2 umq, F2 fourL, auto nr) {
+        const F2 sp = up + um;
+        const F2 Nn = fma2(m2, c, sp);
+        const F2 D = up - um;
+        const F2 base = fma2(D, D, fourL);
+        const F2 Sa = fma2(m2, uq, sp), Sb = fma2(m2, umq, sp);
+        if constexpr (decltype(nr)::value)
+            return Nn * (rsqrt2_nr(fma2(Sa, Sa, base)) + rsqrt2_nr(fma2(Sb, Sb, base)));
+        else
+            return Nn * (rsqrt2(fma2(Sa, Sa, base)) + rsqrt2(fma2(Sb, Sb, base)));
+    };
+    using NO = std::integral_constant<bool, false>;
+    using YES = std::integral_constant<bool, (NR > 0)>;
+    const F2 t1 = pair(E, W, N, S, four, NO{});
+    const F2 t2 = pair(N, S, W, E, four, NO{});
+    const F2 t3 = pair(NE, SW, NW, SE, eight, YES{});
+    const F2 t4 = pair(NW, SE, SW, NE, eight, NO{});
+    return fma2(f2_splat(1.41421356237309505f), t3 + t4, t1 + t2) * f2_splat(0.125f);
+}
+
+template <int TH, int TW, int NR>
+__global__ void __launch_bounds__(256) k_l1_x2(FusedArgs<float> a) {
+    using G = L1Geom<float, TH, TW>;
+    static_assert(G::QW % 2 == 0, "pairs must stay 8-byte aligned");
+    constexpr int PAIRS = G::QW / 2;             // packed pairs per plane row
+    constexpr int ROWS_PER_PASS = 256 / PAIRS;   // plane rows handled per pass
+    static_assert(256 % PAIRS == 0, "");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* su = reinterpret_cast<float*>(smem_raw) + 2;  // 2 guard words: p[-1] at the first pair stays in bounds
+    float* sf = su + 4 * G::PLANE;
+    const int b = blockIdx.z;
+    const int R = blockIdx.y * TH, C = blockIdx.x * TW;
+    const float* uin = a.uin + (long long)b * a.istride;
+    const float* f = a.f + (long long)b * a.istride;
+    float* uout = a.uout + (long long)b * a.istride;
+    const int m = a.m, n = a.n;
+    if (a.st[b].done) {
+        for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
+            const int i = R + e / TW, k = C + e % TW;
+            if (i < m && k < n) uout[(long long)i * n + k] = uin[(long long)i * n + k];
+        }
+        return;
+    }
+    const int r0 = R - G::HALO, c0 = C - G::HALO;
+    const bool border = (r0 < 1) || (c0 < 1) || (r0 + G::RH >= m) || (c0 + G::RW >= n);
+    const bool vec = !border && (n % 4 == 0);
+    if (vec) {
+        // 16-byte loads: 4 consecutive pixels -> two 8-byte pairs of the two column planes
+        constexpr int V4 = G::RW / 4;
+        for (int e = threadIdx.x; e < G::RH * V4; e += blockDim.x) {
+            const int i = e / V4, k = 4 * (e % V4);
+            const long long g = (long long)(r0 + i) * n + (c0 + k);
+            const float4 uv = *reinterpret_cast<const float4*>(uin + g);
+            const float4 fv4 = *reinterpret_cast<const float4*>(f + g);
+            const int p0 = G::idx(i, k), p1 = G::idx(i, k + 1);  // planes (i&1,0) and (i&1,1), word k/2
+            *reinterpret_cast<unsigned long long*>(su + p0) = f2_pack(uv.x, uv.z).v;
+            *reinterpret_cast<unsigned long long*>(su + p1) = f2_pack(uv.y, uv.w).v;
+            *reinterpret_cast<unsigned long long*>(sf + p0) = f2_pack(fv4.x, fv4.z).v;
+            *reinterpret_cast<unsigned long long*>(sf + p1) = f2_pack(fv4.y, fv4.w).v;
+        }
+    } else {
+        for (int e = threadIdx.x; e < G::RH * G::RW; e += blockDim.x) {
+            const int i = e / G::RW, k = e % G::RW;
+            const int gi = r0 + i, gk = c0 + k;
+            if (gi >= 0 && gi < m && gk >= 0 && gk < n) {
+                const long long g = (long long)gi * n + gk;
+                su[G::idx(i, k)] = uin[g];
+                sf[G::idx(i, k)] = f[g];
+            }
+        }
+    }
+    __syncthreads();
+    if (border) l1_reflect_fix<float, TH, TW>(su, r0, c0, m, n);
+    const F2 w2 = f2_splat((float)a.P->w[1][0]);
+    const F2 inv2 = f2_splat((float)(1.0 / a.P->den[1][0]));
+    F2 finite_acc = f2_splat(0.f);  // stays 0 unless a correction is inf/NaN (x*0)
+    const F2 zero2 = f2_splat(0.f);
+    const int prow = threadIdx.x / PAIRS, pj = threadIdx.x % PAIRS;
+    static_for<0, 4>([&](auto cphase) {
+        constexpr int c = decltype(cphase)::value;
+        constexpr int P = c >> 1, Q = c & 1;
+        constexpr int h = 3 - c;
+        // valid region rows/cols of this colour phase: [HALO-h, HALO+T+h)
+        constexpr int i_min = G::HALO - h, i_max = G::HALO + TH + h;  // half-open
+        constexpr int k_min = G::HALO - h, k_max = G::HALO + TW + h;
+        constexpr int qi_lo = (i_min - P + 1) / 2, qi_hi = (i_max - P + 1) / 2;  // 2qi+P in [i_min,i_max)
+        // plane offsets of the neighbours: plane (rp,cq), row shift a, col shift b
+        constexpr int PL_c = (P * 2 + Q) * G::PLANE;
+        constexpr int PL_ns = ((1 - P) * 2 + Q) * G::PLANE;          // N and S live in the other row parity
+        constexpr int PL_ew = (P * 2 + (1 - Q)) * G::PLANE;          // E and W
+        constexpr int PL_d = ((1 - P) * 2 + (1 - Q)) * G::PLANE;     // diagonals
+        constexpr int aN = (P - 1) >> 1, aS = (P + 1) >> 1;          // row shift of N / S
+        constexpr int bW = (Q - 1) >> 1, bE = (Q + 1) >> 1;          // col shift of W / E (one of them is 0)
+        for (int qi = qi_lo + prow; qi < qi_hi; qi += ROWS_PER_PASS) {
+            const int qk = 2 * pj;
+            const int base = qi * G::QW + qk;
+            // aligned pairs (b = 0) and the one extra scalar for the b = +-1 side
+            auto pairEW = [&](int rowoff, int plane, F2& Ev, F2& Wv) {
+                const float* p = su + plane + base + rowoff * G::QW;
+                const F2 al = lds2(p);  // columns qk, qk+1 of that plane
+                float lo, hi;
+                f2_unpack(al, lo, hi);
+                if constexpr (bE == 0) {  // E aligned, W = (p[-1], lo)
+                    Ev = al;
+                    Wv = f2_pack(p[-1], lo);
+                } else {  // W aligned, E = (hi, p[2])
+                    Wv = al;
+                    Ev = f2_pack(hi, p[2]);
+                }
+            };
+            const F2 cv = lds2(su + PL_c + base);
+            const F2 fv = lds2(sf + PL_c + base);
+            const F2 Nv = lds2(su + PL_ns + base + aN * G::QW);
+            const F2 Sv = lds2(su + PL_ns + base + aS * G::QW);
+            F2 Ev, Wv, NEv, NWv, SEv, SWv;
+            pairEW(0, PL_ew, Ev, Wv);
+            pairEW(aN, PL_d, NEv, NWv);
+            pairEW(aS, PL_d, SEv, SWv);
+            const F2 ch = l1_chalf_x2<NR>(cv, Ev, Wv, Nv, Sv, NEv, NWv, SEv, SWv);
+            const F2 corr = fma2(w2, fv - cv, ch) * inv2;  // (c_half + w f*) / (2 + w), f* = f - u
+            F2 nu = cv + corr;
+            float c0v, c1v, n0, n1, k0, k1;
+            f2_unpack(cv, c0v, c1v);
+            f2_unpack(nu, n0, n1);
+            f2_unpack(corr, k0, k1);
+            // validity of the two pixels: phase column range and (border tiles) the image
+            const int i = 2 * qi + P;
+            const int kA = 2 * qk + Q, kB = kA + 2;
+            bool okA = kA >= k_min && kA < k_max, okB = kB >= k_min && kB < k_max;
+            if (border) {
+                const int gi = r0 + i;
+                const bool rin = gi >= 0 && gi < m;
+                okA = okA && rin && (c0 + kA) >= 0 && (c0 + kA) < n;
+                okB = okB && rin && (c0 + kB) >= 0 && (c0 + kB) < n;
+            }
+            finite_acc = fma2(f2_pack(okA ? k0 : 0.f, okB ? k1 : 0.f), zero2, finite_acc);
+            nu = f2_pack(okA ? n0 : c0v, okB ? n1 : c1v);
+            *reinterpret_cast<unsigned long long*>(su + PL_c + base) = nu.v;
+        }
+        __syncthreads();
+        if (border) l1_reflect_fix<float, TH, TW>(su, r0, c0, m, n);
+    });
+    float fa0, fa1;
+    f2_unpack(finite_acc, fa0, fa1);
+    const bool bad = !(isfinite(fa0) && isfinite(fa1));
+    if (__syncthreads_or(bad) && threadIdx.x == 0) a.st[b].bad = 1;
+    const bool vec_out = (R + TH <= m) && (C + TW <= n) && (n % 4 == 0);
+    if (vec_out) {
+        constexpr int V4 = TW / 4;
+        for (int e = threadIdx.x; e < TH * V4; e += blockDim.x) {
+            const int i = e / V4, k = 4 * (e % V4);
+            const int p0 = G::idx(i + G::HALO, k + G::HALO), p1 = G::idx(i + G::HALO, k + G::HALO + 1);
+            float x0, x2, x1, x3;
+            f2_unpack(lds2(su + p0), x0, x2);
+            f2_unpack(lds2(su + p1), x1, x3);
+            *reinterpret_cast<float4*>(uout + (long long)(R + i) * n + (C + k)) = make_float4(x0, x1, x2, x3);
+        }
+    } else {
+        for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
+            const int i = e / TW, k = e % TW;
+            const int gi = R + i, gk = C + k;
+            if (gi < m && gk < n) uout[(long long)gi * n + gk] = su[G::idx(i + G::HALO, k + G::HALO)];
+        }
+    }
+}
+
+}  // namespace cmg

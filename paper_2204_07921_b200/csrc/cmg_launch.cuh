@@ -4,10 +4,13 @@
 
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "cmg_fused.cuh"
 #include "cmg_l1.cuh"
+#include "cmg_l1x2.cuh"
+#include "cmg_coarse.cuh"
 #include "cmg_persist.cuh"
 #include "cmg_plan.h"
 
@@ -257,6 +260,18 @@ struct L1Tile<double> {
 
 template <typename T, int MODE, int PREC>
 void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
+    if constexpr (std::is_same<T, float>::value && MODE == MODE_MEAN && PREC == PREC_FAST) {
+        if (P->l1x2) {  // packed fp32x2 variant
+            constexpr int TH = 56, TW = 56;
+            using G = L1Geom<float, TH, TW>;
+            const size_t smem = sizeof(float) * (2 + 8 * G::PLANE);
+            auto kern = P->l1x2 == 2 ? k_l1_x2<TH, TW, 1> : k_l1_x2<TH, TW, 0>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
+            kern<<<grd, 256, smem, P->stream>>>(a);
+            return;
+        }
+    }
     constexpr int TH = L1Tile<T>::TH, TW = L1Tile<T>::TW;
     using G = L1Geom<T, TH, TW>;
     const size_t smem = 2 * sizeof(T) * 4 * G::PLANE;
@@ -270,8 +285,67 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
     kern<<<grd, 256, smem, P->stream>>>(a);
 }
 
+// shared-memory tile configs of the coarse fused levels (patches per tile
+// side TP, lanes per patch TS, threads per CTA NT)
+template <typename T, int LAYER>
+struct CoarseCfg;
+template <>
+struct CoarseCfg<float, 2> {
+    static constexpr int TP = 32, TS = 1, NT = 256;
+};
+template <>
+struct CoarseCfg<double, 2> {
+    static constexpr int TP = 16, TS = 4, NT = 256;
+};
+template <>
+struct CoarseCfg<float, 3> {
+    static constexpr int TP = 8, TS = 8, NT = 256;
+};
+template <>
+struct CoarseCfg<double, 3> {
+    static constexpr int TP = 4, TS = 8, NT = 128;
+};
+
+template <typename T, int LAYER, int MODE, int PREC>
+void launch_coarse(cmg_plan* P, const FusedArgs<T>& a) {
+    using C = CoarseCfg<T, LAYER>;
+    using G = CoarseGeom<T, LAYER, C::TP>;
+    const size_t smem = 128 + 2 * sizeof(T) * G::CELLS_AL + sizeof(PlaneLin) * (G::NPL + 2) + 16;
+    auto kern = k_coarse_tile<T, LAYER, MODE, PREC, C::TP, C::TS, C::NT>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    const Level& L = P->lv[LAYER];
+    const dim3 grd((L.nj + C::TP - 1) / C::TP, (L.mj + C::TP - 1) / C::TP, P->B);
+    int bi = -1;
+    for (int i = 0; i < 3; ++i)
+        if (a.uin == P->ubuf[i]) bi = i;
+    const bool tma = P->tma_ok[LAYER] && bi >= 0;
+    CUtensorMap dummy;
+    memset(&dummy, 0, sizeof(dummy));
+    kern<<<grd, C::NT, smem, P->stream>>>(a, tma ? P->tmap[LAYER][bi] : dummy, tma ? P->tmap[LAYER][3] : dummy,
+                                          tma ? 1 : 0);
+}
+
+// encoded as box_width * 4096 + box_height
+template <typename T>
+inline int coarse_region_impl(int layer) {
+    using G2 = CoarseGeom<T, 2, CoarseCfg<T, 2>::TP>;
+    using G3 = CoarseGeom<T, 3, CoarseCfg<T, 3>::TP>;
+    return layer == 2 ? G2::BW * 4096 + G2::RD : G3::BW * 4096 + G3::RD;
+}
+
 template <typename T, int MODE, int PREC>
 void dispatch_fused(cmg_plan* P, int layer, const FusedArgs<T>& a) {
+    if (layer >= 2 && P->coarse_tile) {
+        if (layer == 2)
+            launch_coarse<T, 2, MODE, PREC>(P, a);
+        else
+            launch_coarse<T, 3, MODE, PREC>(P, a);
+        return;
+    }
     if (layer == 1) {
         if (P->l1_tile)
             launch_l1_tile<T, MODE, PREC>(P, a);
@@ -279,21 +353,18 @@ void dispatch_fused(cmg_plan* P, int layer, const FusedArgs<T>& a) {
             launch_fused<T, 1, MODE, PREC, 0>(P, a);
     } else if (layer == 2) {
         switch (P->fcfg2) {
-            case 1: launch_fused<T, 2, MODE, PREC, 1>(P, a); break;
             case 2: launch_fused<T, 2, MODE, PREC, 2>(P, a); break;
-            case 3: launch_fused<T, 2, MODE, PREC, 3>(P, a); break;
             default: launch_fused<T, 2, MODE, PREC, 0>(P, a); break;
         }
     } else {
         switch (P->fcfg3) {
-            case 1: launch_fused<T, 3, MODE, PREC, 1>(P, a); break;
             case 2:
                 if (sizeof(T) == 4) {
                     launch_fused<T, 3, MODE, PREC, 2>(P, a);
                     break;
                 }
-                [[fallthrough]];
-            case 3: launch_fused<T, 3, MODE, PREC, 3>(P, a); break;
+                launch_fused<T, 3, MODE, PREC, 0>(P, a);
+                break;
             default: launch_fused<T, 3, MODE, PREC, 0>(P, a); break;
         }
     }
@@ -461,4 +532,8 @@ cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full) {
     template void cmg::enqueue_fused_level<T>(cmg_plan*, int, const void*, void*);  \
     template void cmg::enqueue_energy_ptrs<T>(cmg_plan*, const void*, const void*, bool, double*, int, double*, \
                                               long long, long long);                                   \
-    template void cmg::enqueue_body_fused<T>(cmg_plan*, int, bool);
+    template void cmg::enqueue_body_fused<T>(cmg_plan*, int, bool);                  \
+    template <>                                                                     \
+    int cmg::coarse_region<T>(int layer) {                                          \
+        return cmg::coarse_region_impl<T>(layer);                                   \
+    }

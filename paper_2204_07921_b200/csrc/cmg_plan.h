@@ -2,6 +2,7 @@
 // the host runtime (cmg.cu) and the per-dtype launch units (cmg_f64/f32.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/cmg.h"
@@ -45,7 +46,11 @@ struct cmg_plan {
     int ts2 = 4, ts3 = 16;
     int dbg = 0;
     bool l1_tile = true;
-    int fcfg2 = 0, fcfg3 = 0;  // fused L2/L3 tile variants (FusedCfg)  // dedicated level-1 tile kernel (k_l1_tile) instead of k_level_fused<1>  // diagnostics bits (CMG_DBG), see SweepArgs::dbg  // team sizes (lanes per patch) of levels 2 and 3
+    int l1x2 = 1;  // 1: packed fp32x2 level-1 kernel (fp32 fast mean); 2: + Newton rsqrt on one pair  // packed fp32x2 level-1 kernel for fp32 fast mean mode
+    int fcfg2 = 0, fcfg3 = 0;
+    bool coarse_tile = true;  // k_coarse_tile for fused levels 2-3
+    bool tma_ok[4] = {false, false, false, false};
+    CUtensorMap tmap[4][4];  // [level][buffer 0..2 = u rotation, 3 = f]  // fused L2/L3 tile variants (FusedCfg)  // dedicated level-1 tile kernel (k_l1_tile) instead of k_level_fused<1>  // diagnostics bits (CMG_DBG), see SweepArgs::dbg  // team sizes (lanes per patch) of levels 2 and 3
     // graphs
     cudaGraphExec_t exec = nullptr;
     int gkey = -1;
@@ -59,7 +64,7 @@ struct cmg_plan {
     int enq = 0;  // kernels enqueued since last reset
     // fused-level path (all four colours of a level in one tile kernel)
     bool fused = false;
-    int fuse_mask = 1;  // bit j-1: level j runs as one fused tile kernel (bit 0 required)
+    int fuse_mask = 7;  // bit j-1: level j runs as one fused tile kernel (bit 0 required)
     void* ubuf[3] = {nullptr, nullptr, nullptr};  // rotation buffers (ubuf[0]=u, ubuf[1]=uprev)
     // persistent cooperative path
     bool persist = false;
@@ -86,4 +91,7 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
                          double* raw5, long long e_lo, long long e_hi);
 template <typename T>
 void enqueue_body_fused(cmg_plan* P, int full, bool has_ref);
+template <typename T>
+int coarse_region(int layer);
+bool make_tmap(CUtensorMap* out, const void* base, int esz, int m, int n, int B, int box);
 }  // namespace cmg

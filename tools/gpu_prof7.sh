@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+export CMG_NO_WHILE=1
+python tools/prof_big.py 8192 float32 fast > gpurun_out/plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_l1_x2" -c 1 -o gpurun_out/prof_x2 python tools/prof_big.py 8192 float32 fast > gpurun_out/ncu_full.log 2>&1
+tail -2 gpurun_out/ncu_full.log

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -x -k "fp32 or strips or batch" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log
+timeout 600 python tools/probe_big.py 16384 float32 fast 2>&1 | tail -4
+timeout 300 python bench.py --steps 3 --warmup 3 --config 4 --no-cpu > gpurun_out/b.json 2>&1
+python -c "import json,sys; d=json.load(open('gpurun_out/b.json')); print('cfg4', round(d['ms_per_step'],3), {k: round(v*1000,1) for k,v in d['config']['level_sweep_ms'].items()}, round(d['roofline']['frac'],3))" || tail -3 gpurun_out/b.json
