@@ -113,7 +113,10 @@ void enqueue_cycle(cmg_plan* P, int full, bool has_ref) {
 
 int build_graph(cmg_plan* P, int full, bool has_ref) {
     const int key = full * 2 + (has_ref ? 1 : 0);
-    if (P->exec && P->gkey == key) return CMG_OK;
+    // kernel arguments carry the backward-step constants: rebuild when they change
+    if (P->exec && P->gkey == key && P->galpha == P->hostP.alpha && P->ginner == P->hostP.inner) return CMG_OK;
+    P->galpha = P->hostP.alpha;
+    P->ginner = P->hostP.inner;
     if (P->exec) {
         cudaGraphExecDestroy(P->exec);
         P->exec = nullptr;
@@ -135,9 +138,14 @@ int build_graph(cmg_plan* P, int full, bool has_ref) {
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         CK(cudaStreamBeginCaptureToGraph(P->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
         P->enq = 0;
+        P->cur_cond = P->fused_finalize ? (unsigned long long)h : 0ULL;
         enqueue_cycle(P, full, has_ref);
-        k_cond<<<1, 1, 0, P->stream>>>(h, P->ndone, P->B, P->iters);
-        P->enq += 1;
+        P->cur_cond = 0;
+        if (!P->fused_finalize) {
+            k_cond<<<1, 1, 0, P->stream>>>(h, P->ndone, P->B, P->iters);
+            P->enq += 1;
+            stamp(P, 99);
+        }
         cudaGraph_t outg = nullptr;
         cudaError_t ce = cudaStreamEndCapture(P->stream, &outg);
         if (ce != cudaSuccess) {
@@ -228,6 +236,7 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
     if (rc) return rc;
     SolveParams sp;
     fill_params(P, sp, alpha, eps, max_outer, inner, stop_rule, has_ref, peak);
+    P->hostP = sp;
     CK(cudaMemcpyAsync(P->P, &sp, sizeof(sp), cudaMemcpyHostToDevice, P->stream));
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
     CK(cudaMemsetAsync(P->ndone, 0, sizeof(int) * 2, P->stream));
@@ -286,12 +295,23 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
     CK(cudaEventElapsedTime(&P->dev_ms, P->e0, P->e1));
     std::vector<ImgState> hs(P->B);
     CK(cudaMemcpy(hs.data(), P->st, sizeof(ImgState) * P->B, cudaMemcpyDeviceToHost));
-    if (P->persist || P->fused) {
+    {
         cycles = 0;
         for (int b = 0; b < P->B; ++b)
             cycles = std::max(cycles, hs[b].cycle + ((hs[b].status == ST_DIVERGED || hs[b].status == ST_NONFINITE) ? 1 : 0));
     }
     P->cycles_run = cycles;
+    if (P->stamps) {
+        std::vector<unsigned long long> sb(P->stamps_cap);
+        CK(cudaMemcpy(sb.data(), P->stamps, sizeof(unsigned long long) * P->stamps_cap, cudaMemcpyDeviceToHost));
+        const int cnt = std::min((int)(sb[0] & 0xffffffffu), P->stamps_cap - 1);
+        FILE* fo = fopen(getenv("CMG_STAMPS_FILE") ? getenv("CMG_STAMPS_FILE") : "cmg_stamps.txt", "w");
+        if (fo) {
+            for (int i = 0; i < cnt; ++i) fprintf(fo, "%d %llu\n", (int)(sb[1 + i] & 0xff), sb[1 + i] >> 8);
+            fclose(fo);
+        }
+        CK(cudaMemset(P->stamps, 0, sizeof(unsigned long long) * P->stamps_cap));
+    }
     double* outs[5] = {energy, rel_e, rel_u, psnr, seconds};
     for (int i = 0; i < 5; ++i) {
         if (!outs[i]) continue;
@@ -344,7 +364,7 @@ int cmg_plan_destroy(cmg_plan* P) {
     cudaSetDevice(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     if (P->exec) cudaGraphExecDestroy(P->exec);
-    void* ptrs[] = {P->u, P->uprev, P->ubuf[2], P->f, P->ref, P->upad, P->epad, P->partials, P->st, P->ndone, P->eonly, P->raw5, P->P};
+    void* ptrs[] = {P->u, P->uprev, P->ubuf[2], P->f, P->ref, P->upad, P->epad, P->partials, P->st, P->ndone, P->eonly, P->raw5, P->P, P->stamps, P->tickets};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 5; ++i)
@@ -385,12 +405,38 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     P->use_while = !(nw && nw[0] == '1');
     if (const char* t2 = getenv("CMG_TS2")) P->ts2 = atoi(t2);
     if (const char* t3 = getenv("CMG_TS3")) P->ts3 = atoi(t3);
+    {
+        // level 1 always runs as one fused tile kernel; levels 2-3 only when the
+        // image is large enough that the fused SMEM tiles fill the GPU several
+        // times over (small images are latency-bound: per-colour team kernels win)
+        const int tp2 = dtype == CMG_F64 ? 16 : 32, tp3 = dtype == CMG_F64 ? 4 : 8;
+        // (per-image tile grids must also be large: border tiles cannot use TMA)
+        auto tiles = [&](int s, int tp) {
+            const long long mj = (m + s - 1) / s, nj = (n + s - 1) / s;
+            return ((mj + tp - 1) / tp) * ((nj + tp - 1) / tp);
+        };
+        P->fuse_mask = 1;
+        if (layers >= 2 && tiles(3, tp2) >= 400 && tiles(3, tp2) * batch >= 2048) P->fuse_mask |= 2;
+        if (layers >= 3 && tiles(7, tp3) >= 400 && tiles(7, tp3) * batch >= 8192) P->fuse_mask |= 4;
+    }
     if (const char* fm = getenv("CMG_FUSE_MASK")) P->fuse_mask = atoi(fm) | 1;
     if (const char* dg = getenv("CMG_DBG")) P->dbg = atoi(dg);
+    if (const char* sp = getenv("CMG_STAMPS")) {
+        if (atoi(sp) > 0) {
+            P->stamps_cap = 1 << 16;
+            if (cudaMalloc(&P->stamps, sizeof(unsigned long long) * P->stamps_cap) != cudaSuccess) {
+                P->stamps = nullptr;
+            } else {
+                cudaMemset(P->stamps, 0, sizeof(unsigned long long) * P->stamps_cap);
+            }
+        }
+    }
     if (const char* lt = getenv("CMG_L1_TILE")) P->l1_tile = atoi(lt) != 0;
     if (const char* lx = getenv("CMG_L1X2")) P->l1x2 = atoi(lx);
     if (const char* v2 = getenv("CMG_FCFG2")) P->fcfg2 = atoi(v2);
     if (const char* ct = getenv("CMG_COARSE_TILE")) P->coarse_tile = atoi(ct) != 0;
+    if (const char* cp = getenv("CMG_COOP")) P->coop = atoi(cp) != 0;
+    if (const char* co = getenv("CMG_COOP_OCC")) P->coop_occ = std::max(1, atoi(co));
     if (const char* v3 = getenv("CMG_FCFG3")) P->fcfg3 = atoi(v3);
     auto bail = [&](int rc) {
         cmg_plan_destroy(P);
@@ -464,8 +510,10 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
             P->tma_ok[j] = ok;
         }
     }
+    // energy CTAs per image: row bands of >= 4 rows, ~1184 CTAs in total
     long long want = std::max(1, 1184 / batch);
-    P->nbx = (int)std::max(1LL, std::min(want, (P->N + 255) / 256));
+    if (const char* nb = getenv("CMG_ENERGY_CTAS")) want = std::max(1, atoi(nb) / batch);
+    P->nbx = (int)std::max(1LL, std::min(want, (long long)(m + 3) / 4));
     CKP(cudaMalloc(&P->partials, sizeof(double) * NSUM * (size_t)P->nbx * batch));
     P->pcap = P->nbx * batch;
     CKP(cudaMalloc(&P->st, sizeof(ImgState) * batch));
@@ -473,6 +521,9 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     P->iters = P->ndone + 1;
     CKP(cudaMalloc(&P->eonly, sizeof(double) * batch));
     CKP(cudaMalloc(&P->raw5, sizeof(double) * NSUM * batch));
+    CKP(cudaMalloc(&P->tickets, sizeof(int) * (batch + 1)));
+    CKP(cudaMemset(P->tickets, 0, sizeof(int) * (batch + 1)));
+    if (const char* ff = getenv("CMG_FUSED_FINALIZE")) P->fused_finalize = atoi(ff) != 0;
     CKP(cudaMalloc(&P->P, sizeof(SolveParams)));
 #undef CKP
     *out = P;
@@ -535,6 +586,7 @@ int cmg_sweep_layer(cmg_plan* P, void* u_host, const void* f_host, int layer, do
     const size_t bytes = P->esz * (size_t)P->N * P->B;
     SolveParams sp;
     fill_params(P, sp, alpha, 1.0, 1, inner_iters, 0, false, 1.0);
+    P->hostP = sp;
     CK(cudaMemcpyAsync(P->P, &sp, sizeof(sp), cudaMemcpyHostToDevice, P->stream));
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
     CK(cudaMemcpyAsync(P->u, u_host, bytes, cudaMemcpyHostToDevice, P->stream));
@@ -571,6 +623,7 @@ int cmg_energy(cmg_plan* P, const void* u_host, const void* f_host, double alpha
     const size_t bytes = P->esz * (size_t)P->N * P->B;
     SolveParams sp;
     fill_params(P, sp, alpha, 1.0, 1, 1, 0, false, 1.0);
+    P->hostP = sp;
     CK(cudaMemcpyAsync(P->P, &sp, sizeof(sp), cudaMemcpyHostToDevice, P->stream));
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
     CK(cudaMemcpyAsync(P->u, u_host, bytes, cudaMemcpyHostToDevice, P->stream));
@@ -697,6 +750,7 @@ int cmg_level_step(cmg_plan* P, int layer, int in_index, int out_index, double a
     if (rc) return rc;
     SolveParams sp;
     fill_params(P, sp, alpha, 1.0, 1, inner_iters, 0, false, 1.0);
+    P->hostP = sp;
     CK(cudaMemcpyAsync(P->P, &sp, sizeof(sp), cudaMemcpyHostToDevice, P->stream));
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
     const bool fusedj = P->fused && layer <= 3 && ((P->fuse_mask >> (layer - 1)) & 1);

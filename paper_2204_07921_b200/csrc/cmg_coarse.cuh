@@ -155,7 +155,10 @@ __device__ __forceinline__ T coarse_solve_thread(const Acc& U, const Acc& F, con
         static_for<0, NPL>([&](auto l) { plane_exact<T, decltype(l)::value>(U, ci, cc, uo, &d[decltype(l)::value], nullptr); });
         T sum;
         if (a.single) {
-            sum = pairwise_of<T>(d, NPL);
+            T tmp[NPL];
+#pragma unroll
+            for (int l = 0; l < NPL; ++l) tmp[l] = d[l];
+            sum = pairwise_of<T>(tmp, NPL);
         } else {
             sum = d[0];
 #pragma unroll
@@ -412,6 +415,10 @@ __global__ void __launch_bounds__(NT) k_coarse_tile(FusedArgs<T> a, const __grid
     sa.P = a.P;
     sa.st = a.st;
     sa.dbg = 0;
+    sa.bk.inner = a.P->inner;
+    sa.bk.w0 = a.P->w[LAYER][0];
+    sa.bk.den0 = a.P->den[LAYER][0];
+    sa.bk.inv0 = 1.0 / sa.bk.den0;
     const T w = T(a.P->w[LAYER][0]), den = T(a.P->den[LAYER][0]), inv = T(1.0 / a.P->den[LAYER][0]);
     bool bad = false;
     // pad values of u are refreshed after every phase on border tiles; f's once

@@ -81,6 +81,10 @@ __device__ __forceinline__ void fused_phases(const Acc& U, const Acc& F, T* su, 
     s.P = a.P;
     s.st = a.st;
     s.dbg = 0;
+    s.bk.inner = a.P->inner;
+    s.bk.w0 = a.P->w[LAYER][0];
+    s.bk.den0 = a.P->den[LAYER][0];
+    s.bk.inv0 = 1.0 / s.bk.den0;
     const int tid = threadIdx.x;
     bool bad = false;
 #pragma unroll 1

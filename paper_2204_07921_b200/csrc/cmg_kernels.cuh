@@ -41,6 +41,13 @@ struct SolveParams {
     double den[7][16];  // 2 + w
 };
 
+// backward-step constants of one level, passed BY VALUE in the kernel
+// arguments (constant bank) so the patch solve needs no dependent global load
+struct BackK {
+    int inner;
+    double w0, den0, inv0;
+};
+
 struct ImgState {
     double F;         // last energy
     int cycle;        // index of last trace record
@@ -66,6 +73,7 @@ struct SweepArgs {
     const SolveParams* P;
     ImgState* st;
     int dbg;  // diagnostics: bit0 skip planes, bit1 skip f*, bit2 skip apply, bit3 exit early
+    BackK bk;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -78,7 +86,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // f* of a colour class with a single patch column (NumPy coalesces the patch
 // into one flat pairwise sum) ...
 template <typename T, int S, class Acc>
-__device__ __noinline__ T fstar_flat_sum(const Acc& U, const Acc& F, int R0, int C0) {
+__device__ __noinline__ T fstar_flat_sum(const Acc U, const Acc F, int R0, int C0) {
     using O = X<T>;
     return O::add(T(0), pairwise_small<T>(S * S, [&](int e) {
         return O::sub(F(R0 + e / S, C0 + e % S), U(R0 + e / S, C0 + e % S));
@@ -89,6 +97,25 @@ __device__ __noinline__ T fstar_flat_sum(const Acc& U, const Acc& F, int R0, int
 template <typename T>
 __device__ __noinline__ T pairwise_of(const T* v, int n) {
     return pairwise_any<T>(n, [&](int i) { return v[i]; });
+}
+
+// backward steps (driver.py:212-214, fbs.py:84-90): c_0 = 0, so the common
+// single step is (c_half + w f*) / (2 + w); constants come from the kernel
+// arguments (SweepArgs::bk), further steps from SolveParams
+template <typename T, int LAYER, int PREC>
+__device__ __forceinline__ T backward_steps(T chalf, T fstar, const SweepArgs<T>& a) {
+    using O = X<T>;
+    if (a.bk.inner == 1) {
+        if constexpr (PREC == PREC_FAST)
+            return (chalf + T(a.bk.w0) * fstar) * T(a.bk.inv0);
+        else  // keep the reference's (0 + c_half) so even the sign of zero matches
+            return O::div(O::add(O::add(T(0), chalf), O::mul(T(a.bk.w0), fstar)), T(a.bk.den0));
+    }
+    T c = T(0);
+    const int lay = LAYER > 0 ? LAYER : a.layer;
+    for (int t = 0; t < a.bk.inner; ++t)
+        c = O::div(O::add(O::add(c, chalf), O::mul(T(a.P->w[lay][t]), fstar)), T(a.P->den[lay][t]));
+    return c;
 }
 
 // ---------------------------------------------------------------------------
@@ -131,7 +158,10 @@ __device__ __forceinline__ T patch_solve_ct(const Acc& U, const Acc& F, int R0, 
             static_for<0, NPL>([&](auto l) { plane_exact<T, decltype(l)::value>(U, ci, cc, uo, &d[decltype(l)::value], nullptr); });
             T sum;
             if (a.single) {
-                sum = pairwise_of<T>(d, NPL);
+                T tmp[NPL];
+#pragma unroll
+                for (int l = 0; l < NPL; ++l) tmp[l] = d[l];
+                sum = pairwise_of<T>(tmp, NPL);
             } else {
                 sum = d[0];
 #pragma unroll
@@ -168,11 +198,7 @@ __device__ __forceinline__ T patch_solve_ct(const Acc& U, const Acc& F, int R0, 
         plane_exact_rt<T>(U, ci, cc, uo, PlaneRT::get(star), &chalf, nullptr);
     }
 
-    // backward steps (driver.py:212-214, fbs.py:84-90)
-    T c = T(0);
-    for (int t = 0; t < a.P->inner; ++t)
-        c = O::div(O::add(O::add(c, chalf), O::mul(T(a.P->w[LAYER][t]), fstar)), T(a.P->den[LAYER][t]));
-    return c;
+    return backward_steps<T, LAYER, PREC>(chalf, fstar, a);
 }
 
 template <typename T>
@@ -187,7 +213,7 @@ __device__ __forceinline__ void apply_patch(T* u, int m, int n, int R0, int C0, 
 
 // Border patches (odd reflection) take an out-of-line copy of the solve.
 template <typename T, int LAYER, int MODE, int PREC>
-__device__ __noinline__ T patch_solve_ct_border(const T* u, const T* f, int R0, int C0, const SweepArgs<T>& a) {
+__device__ __forceinline__ T patch_solve_ct_border(const T* u, const T* f, int R0, int C0, const SweepArgs<T>& a) {
     Reflect<T> U{u, a.m, a.n}, F{f, a.m, a.n};
     return patch_solve_ct<T, LAYER, MODE, PREC>(U, F, R0, C0, a);
 }
@@ -355,14 +381,11 @@ __device__ __forceinline__ T patch_solve_team(const Acc& U, const Acc& F, int R0
         if (lane == 0) plane_exact_rt<T>(U, ci, cc, uo, PlaneRT::getg(star), &ph, nullptr);
         chalf = __shfl_sync(FULL, ph, 0, TS);
     }
-    T c = T(0);
-    for (int t = 0; t < a.P->inner; ++t)
-        c = O::div(O::add(O::add(c, chalf), O::mul(T(a.P->w[LAYER][t]), fstar)), T(a.P->den[LAYER][t]));
-    return c;
+    return backward_steps<T, LAYER, PREC>(chalf, fstar, a);
 }
 
 template <typename T, int LAYER, int MODE, int PREC, int TS>
-__device__ __noinline__ T patch_solve_team_border(const T* u, const T* f, int R0, int C0, int lane,
+__device__ __forceinline__ T patch_solve_team_border(const T* u, const T* f, int R0, int C0, int lane,
                                                   const SweepArgs<T>& a) {
     Reflect<T> U{u, a.m, a.n}, F{f, a.m, a.n};
     return patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, a);
@@ -551,86 +574,6 @@ __device__ __forceinline__ A curv_term(A uo, A uE, A uW, A uN, A uS, A uNE, A uS
     return term;
 }
 
-template <typename T, int SRC>
-__global__ void __launch_bounds__(256) k_energy(EnergyArgs a) {
-    using A = T;  // per-pixel precision
-    const int b = blockIdx.y;
-    double acc[NSUM] = {0, 0, 0, 0, 0};
-    if (!a.st[b].done) {
-        const T* u = (const T*)a.u + (long long)b * a.istride;
-        const T* f = (const T*)a.f + (long long)b * a.istride;
-        const T* up = (const T*)a.uprev + (long long)b * a.istride;
-        const T* rf = a.ref ? (const T*)a.ref + (long long)b * a.istride : nullptr;
-        const int n = a.n, m = a.m;
-        const int r_lo = (int)(a.e_lo / n), r_hi = (int)(a.e_hi / n);
-        constexpr int V = 8;  // columns per thread per row (fp32 partial sums of 8 terms)
-        for (int i = r_lo + blockIdx.x; i < r_hi; i += a.nbx) {
-            for (int k0 = threadIdx.x * V; k0 < n; k0 += blockDim.x * V) {
-                A loc[NSUM] = {0, 0, 0, 0, 0};
-#pragma unroll
-                for (int j = 0; j < V; ++j) {
-                    const int k = k0 + j;
-                    if (k < n) {
-                        A c, E, W, N, S, NE, SW, NW, SE;
-                        auto ld = [&](const auto& U) {
-                            c = (A)U(i, k);
-                            E = (A)U(i, k + 1);
-                            W = (A)U(i, k - 1);
-                            N = (A)U(i - 1, k);
-                            S = (A)U(i + 1, k);
-                            NE = (A)U(i - 1, k + 1);
-                            SW = (A)U(i + 1, k - 1);
-                            NW = (A)U(i - 1, k - 1);
-                            SE = (A)U(i + 1, k + 1);
-                        };
-                        if constexpr (SRC == SRC_PADDED) {
-                            ld(Padded<T>{(const T*)a.upad + (long long)b * a.pstride, a.W});
-                        } else {
-                            if (i >= 1 && k >= 1 && i + 1 < m && k + 1 < n)
-                                ld(Direct<T>{u, n});
-                            else
-                                ld(Reflect<T>{u, m, n});
-                        }
-                        loc[0] += curv_term<A>(c, E, W, N, S, NE, SW, NW, SE, a.mode);
-                        const long long e = (long long)i * n + k;
-                        const A d = c - (A)f[e];
-                        loc[1] += d * d;
-                        loc[2] += fabs(c - (A)up[e]);
-                        loc[3] += fabs(c);
-                        if (rf) {
-                            const A dr = c - (A)rf[e];
-                            loc[4] += dr * dr;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int s = 0; s < NSUM; ++s) acc[s] += (double)loc[s];
-            }
-        }
-    }
-    // deterministic block reduction
-    __shared__ double sh[NSUM][32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-    for (int s = 0; s < NSUM; ++s) {
-        double v = acc[s];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if (lane == 0) sh[s][wid] = v;
-    }
-    __syncthreads();
-    if (wid == 0) {
-        const int nw = blockDim.x >> 5;
-#pragma unroll
-        for (int s = 0; s < NSUM; ++s) {
-            double v = lane < nw ? sh[s][lane] : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-            if (lane == 0) a.partials[((long long)b * a.nbx + blockIdx.x) * NSUM + s] = v;
-        }
-    }
-}
-
 struct TraceArgs {
     double* energy;  // [B][cap]
     double* rel_e;
@@ -643,31 +586,31 @@ struct TraceArgs {
     double* raw5;   // raw partial sums [B][5] (strip mode), or nullptr
 };
 
-// One CTA per image: reduce partials in a fixed order, record the trace and
-// apply the stopping rule (driver.py:294-310).
-static __global__ void __launch_bounds__(256) k_finalize(const double* partials, int nbx, const SolveParams* P,
-                                                  ImgState* st, TraceArgs tr, int initial) {
-    const int b = blockIdx.x;
+// Finalize one image (one CTA): reduce its partials in a fixed order, record
+// the trace and apply the stopping rule (driver.py:294-310).  Returns true
+// if the image is (now) done.
+__device__ __forceinline__ void finalize_image(int b, const double* partials, int nbx, const SolveParams* P,
+                                               ImgState* st, const TraceArgs& tr, int initial) {
     ImgState& S = st[b];
     if (!initial && tr.eonly == nullptr && tr.raw5 == nullptr && S.done) return;
-    __shared__ double sh[NSUM][256];
+    __shared__ double shf[NSUM][256];
     double acc[NSUM] = {0, 0, 0, 0, 0};
     for (int i = threadIdx.x; i < nbx; i += blockDim.x)
 #pragma unroll
-        for (int s = 0; s < NSUM; ++s) acc[s] += partials[((long long)b * nbx + i) * NSUM + s];
+        for (int s = 0; s < NSUM; ++s) acc[s] += __ldcg(&partials[((long long)b * nbx + i) * NSUM + s]);
 #pragma unroll
-    for (int s = 0; s < NSUM; ++s) sh[s][threadIdx.x] = acc[s];
+    for (int s = 0; s < NSUM; ++s) shf[s][threadIdx.x] = acc[s];
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w)
 #pragma unroll
-            for (int s = 0; s < NSUM; ++s) sh[s][threadIdx.x] += sh[s][threadIdx.x + w];
+            for (int s = 0; s < NSUM; ++s) shf[s][threadIdx.x] += shf[s][threadIdx.x + w];
         __syncthreads();
     }
     if (threadIdx.x != 0) return;
-    const double curv = sh[0][0], fid = sh[1][0], du = sh[2][0], au = sh[3][0], dr = sh[4][0];
+    const double curv = shf[0][0], fid = shf[1][0], du = shf[2][0], au = shf[3][0], dr = shf[4][0];
     if (tr.raw5) {
-        for (int s = 0; s < NSUM; ++s) tr.raw5[b * NSUM + s] = sh[s][0];
+        for (int s = 0; s < NSUM; ++s) tr.raw5[b * NSUM + s] = shf[s][0];
         return;
     }
     const double F = curv + P->half_alpha * fid;
@@ -694,11 +637,9 @@ static __global__ void __launch_bounds__(256) k_finalize(const double* partials,
         tr.rel_u[base] = __longlong_as_double(0x7ff8000000000000ULL);
         tr.psnr[base] = ps;
         tr.seconds[base] = 0.0;
-        if (!isfinite(F)) {  // the reference records F0 and fails at cycle 1
-        }
         return;
     }
-    const int k = S.cycle + 1;
+    const int kk = S.cycle + 1;
     if (S.bad) {
         S.status = ST_NONFINITE;
         S.done = 1;
@@ -706,7 +647,7 @@ static __global__ void __launch_bounds__(256) k_finalize(const double* partials,
         return;
     }
     if (!isfinite(F)) {
-        tr.energy[base + k] = F;
+        tr.energy[base + kk] = F;
         S.status = ST_DIVERGED;
         S.done = 1;
         atomicAdd(tr.ndone, 1);
@@ -715,22 +656,154 @@ static __global__ void __launch_bounds__(256) k_finalize(const double* partials,
     // rel_err_energy (driver.py:146-150), _rel_u_guarded (driver.py:161-166)
     const double re = (F == 0.0) ? fabs(S.F) : fabs(F - S.F) / fabs(F);
     const double ru = (au == 0.0) ? ((du == 0.0) ? 0.0 : __longlong_as_double(0x7ff0000000000000ULL)) : du / au;
-    tr.energy[base + k] = F;
-    tr.rel_e[base + k] = re;
-    tr.rel_u[base + k] = ru;
-    tr.psnr[base + k] = ps;
-    tr.seconds[base + k] = (double)(now - S.t0) * 1e-9;
+    tr.energy[base + kk] = F;
+    tr.rel_e[base + kk] = re;
+    tr.rel_u[base + kk] = ru;
+    tr.psnr[base + kk] = ps;
+    tr.seconds[base + kk] = (double)(now - S.t0) * 1e-9;
     S.F = F;
-    S.cycle = k;
+    S.cycle = kk;
     const double crit = (P->stop_rule == 0) ? re : ru;
     if (crit <= P->eps) {
         S.status = ST_CONVERGED;
         S.done = 1;
         atomicAdd(tr.ndone, 1);
-    } else if (k >= P->max_outer) {
+    } else if (kk >= P->max_outer) {
         S.status = ST_NOT_CONVERGED;
         S.done = 1;
         atomicAdd(tr.ndone, 1);
+    }
+}
+
+static __global__ void __launch_bounds__(256) k_finalize(const double* partials, int nbx, const SolveParams* P,
+                                                         ImgState* st, TraceArgs tr, int initial) {
+    finalize_image(blockIdx.x, partials, nbx, P, st, tr, initial);
+}
+
+// Energy + finalize in one launch: 32x8 pixel tiles (grid-stride), per-CTA
+// fp64 partials, and the LAST CTA of each image (ticket counter) reduces
+// them in a fixed order and runs finalize_image; the last image to finalize
+// also sets the graph's WHILE condition.  Deterministic regardless of which
+// CTA finishes last.
+struct EnergyFin {
+    TraceArgs tr;
+    const SolveParams* P;
+    ImgState* stw;
+    int* tickets;     // [B] per-image CTA counters (self-resetting)
+    int* img_ticket;  // [1] images finalized this cycle (self-resetting)
+    int initial;
+    unsigned long long cond;  // cudaGraphConditionalHandle (0: none)
+    int B;
+};
+
+template <typename T, int SRC>
+__global__ void __launch_bounds__(256) k_energy(EnergyArgs a, EnergyFin fz) {
+    using A = T;
+    const int b = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int tx = tid & 31, ty = tid >> 5;
+    double acc[NSUM] = {0, 0, 0, 0, 0};
+    if (!a.st[b].done) {
+        const T* u = (const T*)a.u + (long long)b * a.istride;
+        const T* f = (const T*)a.f + (long long)b * a.istride;
+        const T* up = (const T*)a.uprev + (long long)b * a.istride;
+        const T* rf = a.ref ? (const T*)a.ref + (long long)b * a.istride : nullptr;
+        const int n = a.n, m = a.m;
+        const int r_lo = (int)(a.e_lo / n), r_hi = (int)(a.e_hi / n);
+        // each CTA owns a band of rows; a thread walks down its columns keeping
+        // the 3x3 neighbourhood in registers (3 new u loads per pixel)
+        const int rows = r_hi - r_lo;
+        const int band = (rows + a.nbx - 1) / a.nbx;
+        const int i0 = r_lo + blockIdx.x * band, i1 = min(r_hi, i0 + band);
+        for (int k = tid; k < n && i0 < i1; k += blockDim.x) {
+            const bool kin = (k >= 1) && (k + 1 < n);
+            auto ldrow = [&](int i, A& wv, A& cv, A& ev) {
+                if (SRC == SRC_PADDED) {
+                    Padded<T> U{(const T*)a.upad + (long long)b * a.pstride, a.W};
+                    wv = (A)U(i, k - 1);
+                    cv = (A)U(i, k);
+                    ev = (A)U(i, k + 1);
+                } else if (kin && i >= 0 && i < m) {
+                    const T* r = u + (long long)i * n + k;
+                    wv = (A)r[-1];
+                    cv = (A)r[0];
+                    ev = (A)r[1];
+                } else {
+                    Reflect<T> U{u, m, n};
+                    wv = (A)U(i, k - 1);
+                    cv = (A)U(i, k);
+                    ev = (A)U(i, k + 1);
+                }
+            };
+            A nw, nc, ne, cw, cc, ce, sw, sc, se;
+            ldrow(i0 - 1, nw, nc, ne);
+            ldrow(i0, cw, cc, ce);
+            A loc[NSUM] = {0, 0, 0, 0, 0};
+            int cnt = 0;
+            for (int i = i0; i < i1; ++i) {
+                ldrow(i + 1, sw, sc, se);
+                const long long e = (long long)i * n + k;
+                const A fv = (A)f[e], pv = (A)up[e];
+                loc[0] += curv_term<A>(cc, ce, cw, nc, sc, ne, sw, nw, se, a.mode);
+                const A d = cc - fv;
+                loc[1] += d * d;
+                loc[2] += fabs(cc - pv);
+                loc[3] += fabs(cc);
+                if (rf) {
+                    const A dr = cc - (A)rf[e];
+                    loc[4] += dr * dr;
+                }
+                if (++cnt == 8) {  // fp32 images: short partial sums, then fp64
+#pragma unroll
+                    for (int s = 0; s < NSUM; ++s) {
+                        acc[s] += (double)loc[s];
+                        loc[s] = A(0);
+                    }
+                    cnt = 0;
+                }
+                nw = cw; nc = cc; ne = ce;
+                cw = sw; cc = sc; ce = se;
+            }
+#pragma unroll
+            for (int s = 0; s < NSUM; ++s) acc[s] += (double)loc[s];
+        }
+    }
+    // deterministic block reduction -> partials[b][blockIdx.x]
+    __shared__ double sh[NSUM][32];
+    __shared__ int last;
+    const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int s = 0; s < NSUM; ++s) {
+        double v = acc[s];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) sh[s][wid] = v;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+#pragma unroll
+        for (int s = 0; s < NSUM; ++s) {
+            double v = lane < nw ? sh[s][lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) a.partials[((long long)b * a.nbx + blockIdx.x) * NSUM + s] = v;
+        }
+    }
+    if (fz.tickets == nullptr) return;  // finalize launched separately
+    __threadfence();
+    if (tid == 0) last = (atomicAdd(&fz.tickets[b], 1) == a.nbx - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (tid == 0) fz.tickets[b] = 0;
+    finalize_image(b, a.partials, a.nbx, fz.P, fz.stw, fz.tr, fz.initial);
+    if (fz.cond == 0ULL || tid != 0) return;
+    __threadfence();
+    if (atomicAdd(fz.img_ticket, 1) == fz.B - 1) {
+        *fz.img_ticket = 0;
+        __threadfence();
+        cudaGraphSetConditional((cudaGraphConditionalHandle)fz.cond, (*((volatile int*)fz.tr.ndone) < fz.B) ? 1u : 0u);
     }
 }
 

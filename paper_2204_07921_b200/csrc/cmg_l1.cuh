@@ -115,7 +115,10 @@ __device__ __forceinline__ T l1_correction(const QuadAcc<T, TH, TW, P, Q>& A, T 
             static_for<0, 8>([&](auto l) { plane_exact<T, decltype(l)::value>(acc, 0, 0, c, &d[decltype(l)::value], nullptr); });
             T sum;
             if (single) {
-                sum = pairwise_of<T>(d, 8);
+                T tmp[8];
+#pragma unroll
+                for (int l = 0; l < 8; ++l) tmp[l] = d[l];
+                sum = pairwise_of<T>(tmp, 8);
             } else {
                 sum = d[0];
 #pragma unroll

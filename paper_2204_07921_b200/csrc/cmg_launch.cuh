@@ -103,6 +103,10 @@ void enqueue_sweep(cmg_plan* P, int layer, int color) {
     a.P = P->P;
     a.st = P->st;
     a.dbg = P->dbg;
+    a.bk.inner = P->hostP.inner;
+    a.bk.w0 = P->hostP.w[layer][0];
+    a.bk.den0 = P->hostP.den[layer][0];
+    a.bk.inv0 = 1.0 / P->hostP.den[layer][0];
     const bool padded = L.general;
     if (layer <= 3) {
         if (P->mode == CMG_MODE_GAUSS)
@@ -126,6 +130,7 @@ void enqueue_sweep(cmg_plan* P, int layer, int color) {
         }
     }
     P->enq += 1;
+    stamp(P, 10 * layer + color);
 }
 
 template <typename T>
@@ -165,10 +170,6 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
     ea.e_hi = e_hi < 0 ? P->N : e_hi;
     ea.partials = P->partials;
     ea.st = P->st;
-    if (P->egeneral)
-        k_energy<T, SRC_PADDED><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea);
-    else
-        k_energy<T, SRC_INPLACE><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea);
     TraceArgs ta;
     ta.energy = P->tr[0];
     ta.rel_e = P->tr[1];
@@ -179,8 +180,26 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
     ta.ndone = P->ndone;
     ta.eonly = eonly;
     ta.raw5 = raw5;
-    k_finalize<<<P->B, 256, 0, P->stream>>>(P->partials, P->nbx, P->P, P->st, ta, initial);
-    P->enq += 2;
+    EnergyFin fz;
+    fz.tr = ta;
+    fz.P = P->P;
+    fz.stw = P->st;
+    fz.tickets = P->fused_finalize ? P->tickets : nullptr;
+    fz.img_ticket = P->tickets + P->B;
+    fz.initial = initial;
+    fz.cond = P->cur_cond;
+    fz.B = P->B;
+    if (P->egeneral)
+        k_energy<T, SRC_PADDED><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea, fz);
+    else
+        k_energy<T, SRC_INPLACE><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea, fz);
+    stamp(P, 90);
+    if (!P->fused_finalize) {
+        k_finalize<<<P->B, 256, 0, P->stream>>>(P->partials, P->nbx, P->P, P->st, ta, initial);
+        P->enq += 1;
+        stamp(P, 91);
+    }
+    P->enq += 1;
 }
 
 template <typename T>
@@ -397,6 +416,7 @@ void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
     else
         dispatch_fused<T, MODE_MEAN, PREC_EXACT>(P, layer, a);
     P->enq += 1;
+    stamp(P, 100 + layer);
 }
 
 // Two V-cycles per graph body with a 3-buffer rotation: fused levels write
@@ -417,7 +437,18 @@ void enqueue_body_fused(cmg_plan* P, int full, bool has_ref) {
         const int target = (half == 0) ? 1 : 0;
         int other = 3 - prev - target;
         bool first = true;
+        std::vector<int> pending;  // consecutive non-fused coarse levels -> one cooperative kernel
+        auto flush = [&]() {
+            if (pending.empty()) return;
+            enqueue_coop<T>(P, P->ubuf[cur], pending.data(), (int)pending.size());
+            pending.clear();
+        };
         for (int j : seq) {
+            if (P->coop && !fusedj(j) && j >= 2 && !P->lv[j].general) {
+                pending.push_back(j);
+                continue;
+            }
+            flush();
             if (fusedj(j)) {
                 int out;
                 if (first) {
@@ -435,6 +466,7 @@ void enqueue_body_fused(cmg_plan* P, int full, bool has_ref) {
                 P->u = save;
             }
         }
+        flush();
         enqueue_energy_ptrs<T>(P, P->ubuf[cur], P->ubuf[prev], has_ref, nullptr, 0, nullptr, 0, -1);
     }
 }
@@ -514,6 +546,64 @@ cudaError_t persist_launch_v(cmg_plan* P, bool has_ref, int full) {
     return e;
 }
 
+// cooperative launch of levels seq[0..nseq) (all >= 2) in place on buffer u
+template <typename T, int MODE, int PREC>
+void coop_launch_v(cmg_plan* P, void* u, const int* seq, int nseq) {
+    auto kern = k_coarse_coop<T, MODE, PREC, 4, 16>;
+    PersistArgs a;
+    memset(&a, 0, sizeof(a));
+    a.u = u;
+    a.f = P->f;
+    a.N = P->N;
+    a.m = P->m;
+    a.n = P->n;
+    a.B = P->B;
+    a.nseq = nseq;
+    for (int i = 0; i < nseq; ++i) a.seq[i] = seq[i];
+    for (int j = 1; j <= P->layers; ++j) {
+        const Level& L = P->lv[j];
+        a.side[j] = L.s;
+        for (int c = 0; c < 4; ++c) {
+            a.hc[j][c] = (L.mj - (c >> 1) + 1) / 2;
+            a.wc[j][c] = (L.nj - (c & 1) + 1) / 2;
+        }
+    }
+    a.P = P->P;
+    a.st = P->st;
+    const size_t smem = 16 * ((P->B * sizeof(int) + 15) / 16) + sizeof(T) * (64 + 256 + 2);
+    static int grid = 0;  // per instantiation (one device per process in practice)
+    if (grid == 0) {
+        int nb = 0, dev = 0, nsm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 256, smem);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        grid = nsm * std::max(1, std::min(nb, P->coop_occ));
+    }
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = P->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a);
+    P->enq += 1;
+}
+
+template <typename T>
+void enqueue_coop(cmg_plan* P, void* u, const int* seq, int nseq) {
+    if (P->mode == CMG_MODE_GAUSS)
+        coop_launch_v<T, MODE_GAUSS, PREC_EXACT>(P, u, seq, nseq);
+    else if (P->prec == CMG_PREC_FAST)
+        coop_launch_v<T, MODE_MEAN, PREC_FAST>(P, u, seq, nseq);
+    else
+        coop_launch_v<T, MODE_MEAN, PREC_EXACT>(P, u, seq, nseq);
+}
+
 template <typename T>
 cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full) {
     if (P->mode == CMG_MODE_GAUSS) return persist_launch_v<T, MODE_GAUSS, PREC_EXACT>(P, has_ref, full);
@@ -533,6 +623,7 @@ cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full) {
     template void cmg::enqueue_energy_ptrs<T>(cmg_plan*, const void*, const void*, bool, double*, int, double*, \
                                               long long, long long);                                   \
     template void cmg::enqueue_body_fused<T>(cmg_plan*, int, bool);                  \
+    template void cmg::enqueue_coop<T>(cmg_plan*, void*, const int*, int);           \
     template <>                                                                     \
     int cmg::coarse_region<T>(int layer) {                                          \
         return cmg::coarse_region_impl<T>(layer);                                   \

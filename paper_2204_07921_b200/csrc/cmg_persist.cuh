@@ -62,6 +62,10 @@ __device__ __forceinline__ SweepArgs<T> make_sweep_args(const PersistArgs& a, in
     s.P = a.P;
     s.st = a.st;
     s.dbg = 0;
+    s.bk.inner = a.P->inner;
+    s.bk.w0 = a.P->w[layer][0];
+    s.bk.den0 = a.P->den[layer][0];
+    s.bk.inv0 = 1.0 / s.bk.den0;
     return s;
 }
 
@@ -393,6 +397,42 @@ __global__ void __launch_bounds__(256) k_persist(PersistArgs a) {
         int running = 0;
         for (int b = threadIdx.x; b < a.B; b += blockDim.x) running |= !sdone[b];
         if (!__syncthreads_or(running)) break;
+    }
+}
+
+}  // namespace cmg
+
+namespace cmg {
+
+// Levels >= 2 of one V-cycle segment (e.g. [2, 3]) as ONE cooperative kernel:
+// each colour of each level is a grid-wide phase (team-per-patch, in place on
+// a.u) separated by grid barriers -- replaces 4 launches per level when the
+// image is small enough that a colour sweep is latency-bound.
+template <typename T, int MODE, int PREC, int TS2, int TS3>
+__global__ void __launch_bounds__(256) k_coarse_coop(PersistArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    int* sdone = reinterpret_cast<int*>(smem);
+    T* sh_rows = reinterpret_cast<T*>(smem + 16 * ((a.B * sizeof(int) + 15) / 16));
+    T* sh_vals = sh_rows + 64;
+    T* sh_c = sh_vals + 256;
+    cg::grid_group grid = cg::this_grid();
+    for (int b = threadIdx.x; b < a.B; b += blockDim.x) sdone[b] = a.st[b].done;
+    __syncthreads();
+    bool first = true;
+    for (int si = 0; si < a.nseq; ++si) {
+        const int j = a.seq[si];
+        for (int c = 0; c < 4; ++c) {
+            if (a.hc[j][c] <= 0 || a.wc[j][c] <= 0) continue;
+            if (!first) grid.sync();
+            first = false;
+            const SweepArgs<T> s = make_sweep_args<T>(a, j, c);
+            if (j == 2)
+                phase_team<T, 2, MODE, PREC, TS2>(s, a.B, sdone);
+            else if (j == 3)
+                phase_team<T, 3, MODE, PREC, TS3>(s, a.B, sdone);
+            else
+                phase_bpp<T, MODE>(s, a.B, sdone, sh_rows, sh_vals, sh_c);
+        }
     }
 }
 

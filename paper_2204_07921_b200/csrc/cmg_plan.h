@@ -40,15 +40,25 @@ struct cmg_plan {
     double* eonly = nullptr;
     double* raw5 = nullptr;  // [B][5] strip-mode partial sums
     cmg::SolveParams* P = nullptr;
+    cmg::SolveParams hostP;  // host copy of the current parameters (kernel-argument constants)
+    double galpha = -1.0;     // parameters baked into the cached graph
+    int ginner = -1;
     double* tr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     int cap = 0;
     // kernel variants
     int ts2 = 4, ts3 = 16;
     int dbg = 0;
+    bool fused_finalize = true;       // energy kernel's last CTA runs the finalize (+ WHILE condition)
+    int* tickets = nullptr;           // [B] + 1 counters of that scheme
+    unsigned long long cur_cond = 0;  // conditional handle while capturing the WHILE body
+    unsigned long long* stamps = nullptr;  // CMG_STAMPS diagnostics buffer
+    int stamps_cap = 0;
     bool l1_tile = true;
     int l1x2 = 1;  // 1: packed fp32x2 level-1 kernel (fp32 fast mean); 2: + Newton rsqrt on one pair  // packed fp32x2 level-1 kernel for fp32 fast mean mode
     int fcfg2 = 0, fcfg3 = 0;
     bool coarse_tile = true;  // k_coarse_tile for fused levels 2-3
+    bool coop = false;        // cooperative kernel for runs of non-fused coarse levels
+    int coop_occ = 4;         // max CTAs per SM of that kernel
     bool tma_ok[4] = {false, false, false, false};
     CUtensorMap tmap[4][4];  // [level][buffer 0..2 = u rotation, 3 = f]  // fused L2/L3 tile variants (FusedCfg)  // dedicated level-1 tile kernel (k_l1_tile) instead of k_level_fused<1>  // diagnostics bits (CMG_DBG), see SweepArgs::dbg  // team sizes (lanes per patch) of levels 2 and 3
     // graphs
@@ -74,6 +84,21 @@ struct cmg_plan {
 };
 
 namespace cmg {
+// diagnostics: a 1-thread kernel that appends %globaltimer to a device buffer
+// (CMG_STAMPS=1); placed after every node of the cycle to attribute time
+static __global__ void k_stamp(unsigned long long* buf, int cap, int tag) {
+    const int i = atomicAdd(reinterpret_cast<int*>(buf), 1);
+    if (i + 1 < cap) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        buf[1 + i] = (t << 8) | (unsigned)tag;
+    }
+}
+
+inline void stamp(cmg_plan* P, int tag) {
+    if (P->stamps) k_stamp<<<1, 1, 0, P->stream>>>(P->stamps, P->stamps_cap, tag);
+}
+
 template <typename T>
 void enqueue_sweep(cmg_plan* P, int layer, int color);
 template <typename T>
@@ -93,5 +118,7 @@ template <typename T>
 void enqueue_body_fused(cmg_plan* P, int full, bool has_ref);
 template <typename T>
 int coarse_region(int layer);
+template <typename T>
+void enqueue_coop(cmg_plan* P, void* u, const int* seq, int nseq);
 bool make_tmap(CUtensorMap* out, const void* base, int esz, int m, int n, int B, int box);
 }  // namespace cmg
