@@ -71,11 +71,10 @@ def test_energy_vs_reference(sweeps):
     meta, arr = sweeps
     for c in meta["energies"]:
         k = c["key"]
-        u, f = arr[f"{k}_u"], arr[f"{k}_f"]
+        u, f = np.ascontiguousarray(arr[f"{k}_u"]), np.ascontiguousarray(arr[f"{k}_f"])
         p = _plan(u.shape[0], u.shape[1], c["mode"], layers=1)
         out = np.zeros(1)
-        rc = N.lib().cmg_energy(p.handle, N.ptr(np.ascontiguousarray(u)), N.ptr(np.ascontiguousarray(f)), 0.06,
-                                N.dptr(out))
+        rc = N.lib().cmg_energy(p.handle, N.ptr(u), N.ptr(f), 0.06, N.dptr(out))
         assert rc == 0, N.last_error()
         assert abs(out[0] - c["energy"]) <= ENERGY_RTOL_EXACT * abs(c["energy"]), (c, out[0])
 
