@@ -114,8 +114,9 @@ int cmg_plan_stats(cmg_plan* plan, long long* kernel_launches, int* cycles_run, 
 /*
  * Time one sweep kernel with CUDA events on the plan's stream:
  * `reps` launches of the level-`layer` colour-`color` kernel (color < 0: all
- * four colours of the level) on the data left by the last solve.  Writes the
- * mean duration per launch in milliseconds.  Used by bench.py's roofline.
+ * four colours of the level; layer 0: the energy + finalize kernel) on the
+ * data left by the last solve.  Writes the mean duration per launch in
+ * milliseconds.  Used by bench.py's roofline.
  */
 int cmg_time_sweep(cmg_plan* plan, int layer, int color, int reps, double* ms_per_launch);
 

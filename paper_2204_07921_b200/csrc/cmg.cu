@@ -240,7 +240,7 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
     CK(cudaMemcpyAsync(P->P, &sp, sizeof(sp), cudaMemcpyHostToDevice, P->stream));
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
     CK(cudaMemsetAsync(P->ndone, 0, sizeof(int) * 2, P->stream));
-    int cycles = 0;
+    int cycles = 0, bodies = 0, init_launches = 0;
     if (P->persist) {
         CK(cudaEventRecord(P->e0, P->stream));
         P->enq = 0;
@@ -251,8 +251,10 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
         CK(cudaStreamSynchronize(P->stream));
         P->launches = P->enq;
     } else {
-        rc = build_graph(P, full, has_ref);
-        if (rc) return rc;
+        if (!P->no_graph) {
+            rc = build_graph(P, full, has_ref);
+            if (rc) return rc;
+        }
         CK(cudaEventRecord(P->e0, P->stream));
         P->enq = 0;
         const size_t bytes = P->esz * (size_t)P->N * P->B;
@@ -266,19 +268,28 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
             enqueue_energy_ptrs<float>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1, nullptr, 0, -1);
         }
         CK(cudaGetLastError());
-        const int init_launches = P->enq;
+        init_launches = P->enq;
         if (P->use_while) {
             CK(cudaGraphLaunch(P->exec, P->stream));
             CK(cudaEventRecord(P->e1, P->stream));
             CK(cudaStreamSynchronize(P->stream));
-            CK(cudaMemcpy(&cycles, P->iters, sizeof(int), cudaMemcpyDeviceToHost));
+            bodies = -1;  // counted from the per-image cycle counters below
         } else {
             int chunk = 1, launched = 0;
             const int per = P->fused ? 2 : 1;
             const int maxb = (max_outer + per - 1) / per;
             while (true) {
                 const int c = std::min(chunk, maxb - launched);
-                for (int i = 0; i < c; ++i) CK(cudaGraphLaunch(P->exec, P->stream));
+                for (int i = 0; i < c; ++i) {
+                    if (P->no_graph) {  // profiling mode: plain stream launches, same kernels
+                        const int e0 = P->enq;
+                        enqueue_cycle(P, full, has_ref);
+                        P->nodes_per_cycle = P->enq - e0;
+                        CK(cudaGetLastError());
+                    } else {
+                        CK(cudaGraphLaunch(P->exec, P->stream));
+                    }
+                }
                 launched += c;
                 int nd = 0;
                 CK(cudaMemcpyAsync(&nd, P->ndone, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
@@ -288,9 +299,8 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
             }
             CK(cudaEventRecord(P->e1, P->stream));
             CK(cudaStreamSynchronize(P->stream));
-            cycles = launched;
+            bodies = launched;
         }
-        P->launches = (long long)init_launches + (long long)cycles * P->nodes_per_cycle;
     }
     CK(cudaEventElapsedTime(&P->dev_ms, P->e0, P->e1));
     std::vector<ImgState> hs(P->B);
@@ -301,6 +311,13 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
             cycles = std::max(cycles, hs[b].cycle + ((hs[b].status == ST_DIVERGED || hs[b].status == ST_NONFINITE) ? 1 : 0));
     }
     P->cycles_run = cycles;
+    if (!P->persist) {
+        // kernels executed on the device: set-up kernels + every kernel node of
+        // every WHILE-body replay (a body holds 2 cycles on the fused path)
+        const int per = P->fused ? 2 : 1;
+        if (bodies < 0) bodies = std::max(1, (cycles + per - 1) / per);
+        P->launches = (long long)init_launches + (long long)bodies * P->nodes_per_cycle;
+    }
     if (P->stamps) {
         std::vector<unsigned long long> sb(P->stamps_cap);
         CK(cudaMemcpy(sb.data(), P->stamps, sizeof(unsigned long long) * P->stamps_cap, cudaMemcpyDeviceToHost));
@@ -403,6 +420,10 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     P->N = (long long)m * n;
     const char* nw = getenv("CMG_NO_WHILE");
     P->use_while = !(nw && nw[0] == '1');
+    if (const char* ng = getenv("CMG_NO_GRAPH")) {
+        P->no_graph = ng[0] == '1';
+        if (P->no_graph) P->use_while = false;
+    }
     if (const char* t2 = getenv("CMG_TS2")) P->ts2 = atoi(t2);
     if (const char* t3 = getenv("CMG_TS3")) P->ts3 = atoi(t3);
     {
@@ -514,6 +535,27 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     long long want = std::max(1, 1184 / batch);
     if (const char* nb = getenv("CMG_ENERGY_CTAS")) want = std::max(1, atoi(nb) / batch);
     P->nbx = (int)std::max(1LL, std::min(want, (long long)(m + 3) / 4));
+    // rows streamed by bulk async copies (k_energy_bulk): 16-byte aligned rows
+    {
+        const char* eb = getenv("CMG_EBULK");
+        // large jobs only: below ~4M pixels the pass is latency-bound and the
+        // row-band kernel (no pipeline fill) is faster
+        const bool big = (long long)batch * m * n >= (4LL << 20);
+        const bool on = (eb ? atoi(eb) != 0 : big) && !P->egeneral && ((size_t)n * P->esz) % 16 == 0;
+        if (on) {
+            if (dtype == CMG_F32)
+                P->eb_px = n > 512 ? 4 : (n > 256 ? 2 : 1);
+            else
+                P->eb_px = n > 256 ? 2 : 1;
+            if (const char* ns = getenv("CMG_EBULK_NS")) P->eb_ns = std::min(8, std::max(2, atoi(ns)));
+            const int nb = dtype == CMG_F64 ? energy_bulk_cfg<double>(batch, m, n, P->eb_px, P->eb_ns, &P->eb_H)
+                                            : energy_bulk_cfg<float>(batch, m, n, P->eb_px, P->eb_ns, &P->eb_H);
+            if (!getenv("CMG_ENERGY_CTAS")) P->nbx = nb;
+        }
+    }
+    if (getenv("CMG_VERBOSE"))
+        fprintf(stderr, "cmg plan %dx%dx%d: energy CTAs/image %d (bulk px %d ns %d H %d), fused L2 %d L3 %d\n", m,
+                n, batch, P->nbx, P->eb_px, P->eb_ns, P->eb_H, (P->fuse_mask >> 1) & 1, (P->fuse_mask >> 2) & 1);
     CKP(cudaMalloc(&P->partials, sizeof(double) * NSUM * (size_t)P->nbx * batch));
     P->pcap = P->nbx * batch;
     CKP(cudaMalloc(&P->st, sizeof(ImgState) * batch));
@@ -660,11 +702,18 @@ int cmg_plan_stats(cmg_plan* P, long long* kernel_launches, int* cycles_run, dou
 
 int cmg_time_sweep(cmg_plan* P, int layer, int color, int reps, double* ms_per_launch) {
     if (!P || !ms_per_launch) return fail(CMG_EINVAL, "NULL argument");
-    if (layer < 1 || layer > P->layers || color > 3 || reps < 1) return fail(CMG_EINVAL, "bad arguments");
+    if (layer < 0 || layer > P->layers || color > 3 || reps < 1) return fail(CMG_EINVAL, "bad arguments");
     int rc = set_device(P);
     if (rc) return rc;
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
     auto one = [&]() {
+        if (layer == 0) {  // the energy + finalize kernel (energy-only output)
+            if (P->dtype == CMG_F64)
+                enqueue_energy_ptrs<double>(P, P->ubuf[0], P->ubuf[1], false, P->eonly, 0, nullptr, 0, -1);
+            else
+                enqueue_energy_ptrs<float>(P, P->ubuf[0], P->ubuf[1], false, P->eonly, 0, nullptr, 0, -1);
+            return;
+        }
         if (P->fused && layer <= 3 && ((P->fuse_mask >> (layer - 1)) & 1)) {  // production fused kernel
             if (P->dtype == CMG_F64)
                 enqueue_fused_level<double>(P, layer, P->ubuf[0], P->ubuf[2]);

@@ -593,18 +593,22 @@ __device__ __forceinline__ void finalize_image(int b, const double* partials, in
                                                ImgState* st, const TraceArgs& tr, int initial) {
     ImgState& S = st[b];
     if (!initial && tr.eonly == nullptr && tr.raw5 == nullptr && S.done) return;
+    // the first 256 threads reduce (any block size >= 256 may call this)
     __shared__ double shf[NSUM][256];
+    const int tid = threadIdx.x;
     double acc[NSUM] = {0, 0, 0, 0, 0};
-    for (int i = threadIdx.x; i < nbx; i += blockDim.x)
+    if (tid < 256) {
+        for (int i = tid; i < nbx; i += 256)
 #pragma unroll
-        for (int s = 0; s < NSUM; ++s) acc[s] += __ldcg(&partials[((long long)b * nbx + i) * NSUM + s]);
+            for (int s = 0; s < NSUM; ++s) acc[s] += __ldcg(&partials[((long long)b * nbx + i) * NSUM + s]);
 #pragma unroll
-    for (int s = 0; s < NSUM; ++s) shf[s][threadIdx.x] = acc[s];
+        for (int s = 0; s < NSUM; ++s) shf[s][tid] = acc[s];
+    }
     __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w)
+    for (int w = 128; w > 0; w >>= 1) {
+        if (tid < w)
 #pragma unroll
-            for (int s = 0; s < NSUM; ++s) shf[s][threadIdx.x] += shf[s][threadIdx.x + w];
+            for (int s = 0; s < NSUM; ++s) shf[s][tid] += shf[s][tid + w];
         __syncthreads();
     }
     if (threadIdx.x != 0) return;
@@ -696,6 +700,50 @@ struct EnergyFin {
     int B;
 };
 
+// deterministic CTA reduction of the five sums -> partials[b][blockIdx.x];
+// the last CTA of the image (ticket) finalizes it, and the last image sets
+// the graph's WHILE condition
+__device__ __forceinline__ void energy_reduce_finalize(const double (&acc)[NSUM], const EnergyArgs& a,
+                                                       const EnergyFin& fz, int b) {
+    const int tid = threadIdx.x;
+    __shared__ double sh[NSUM][32];
+    __shared__ int last;
+    const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int s = 0; s < NSUM; ++s) {
+        double v = acc[s];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) sh[s][wid] = v;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+#pragma unroll
+        for (int s = 0; s < NSUM; ++s) {
+            double v = lane < nw ? sh[s][lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) a.partials[((long long)b * a.nbx + blockIdx.x) * NSUM + s] = v;
+        }
+    }
+    if (fz.tickets == nullptr) return;  // finalize launched separately
+    __threadfence();
+    if (tid == 0) last = (atomicAdd(&fz.tickets[b], 1) == a.nbx - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (tid == 0) fz.tickets[b] = 0;
+    finalize_image(b, a.partials, a.nbx, fz.P, fz.stw, fz.tr, fz.initial);
+    if (fz.cond == 0ULL || tid != 0) return;
+    __threadfence();
+    if (atomicAdd(fz.img_ticket, 1) == fz.B - 1) {
+        *fz.img_ticket = 0;
+        __threadfence();
+        cudaGraphSetConditional((cudaGraphConditionalHandle)fz.cond, (*((volatile int*)fz.tr.ndone) < fz.B) ? 1u : 0u);
+    }
+}
+
 template <typename T, int SRC>
 __global__ void __launch_bounds__(256) k_energy(EnergyArgs a, EnergyFin fz) {
     using A = T;
@@ -768,43 +816,7 @@ __global__ void __launch_bounds__(256) k_energy(EnergyArgs a, EnergyFin fz) {
             for (int s = 0; s < NSUM; ++s) acc[s] += (double)loc[s];
         }
     }
-    // deterministic block reduction -> partials[b][blockIdx.x]
-    __shared__ double sh[NSUM][32];
-    __shared__ int last;
-    const int lane = tid & 31, wid = tid >> 5;
-#pragma unroll
-    for (int s = 0; s < NSUM; ++s) {
-        double v = acc[s];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if (lane == 0) sh[s][wid] = v;
-    }
-    __syncthreads();
-    if (wid == 0) {
-        const int nw = blockDim.x >> 5;
-#pragma unroll
-        for (int s = 0; s < NSUM; ++s) {
-            double v = lane < nw ? sh[s][lane] : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-            if (lane == 0) a.partials[((long long)b * a.nbx + blockIdx.x) * NSUM + s] = v;
-        }
-    }
-    if (fz.tickets == nullptr) return;  // finalize launched separately
-    __threadfence();
-    if (tid == 0) last = (atomicAdd(&fz.tickets[b], 1) == a.nbx - 1);
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    if (tid == 0) fz.tickets[b] = 0;
-    finalize_image(b, a.partials, a.nbx, fz.P, fz.stw, fz.tr, fz.initial);
-    if (fz.cond == 0ULL || tid != 0) return;
-    __threadfence();
-    if (atomicAdd(fz.img_ticket, 1) == fz.B - 1) {
-        *fz.img_ticket = 0;
-        __threadfence();
-        cudaGraphSetConditional((cudaGraphConditionalHandle)fz.cond, (*((volatile int*)fz.tr.ndone) < fz.B) ? 1u : 0u);
-    }
+    energy_reduce_finalize(acc, a, fz, b);
 }
 
 // ---------------------------------------------------------------------------

@@ -11,6 +11,7 @@
 #include "cmg_l1.cuh"
 #include "cmg_l1x2.cuh"
 #include "cmg_coarse.cuh"
+#include "cmg_energy_bulk.cuh"
 #include "cmg_persist.cuh"
 #include "cmg_plan.h"
 
@@ -191,6 +192,15 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
     fz.B = P->B;
     if (P->egeneral)
         k_energy<T, SRC_PADDED><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea, fz);
+    else if (P->eb_px == 1)
+        k_energy_bulk<T, 1><<<dim3(P->nbx, P->B), 288, eb_smem_bytes<T, 1>(P->eb_ns), P->stream>>>(ea, fz, P->eb_H,
+                                                                                                   P->eb_ns);
+    else if (P->eb_px == 2)
+        k_energy_bulk<T, 2><<<dim3(P->nbx, P->B), 288, eb_smem_bytes<T, 2>(P->eb_ns), P->stream>>>(ea, fz, P->eb_H,
+                                                                                                   P->eb_ns);
+    else if (std::is_same<T, float>::value && P->eb_px == 4)
+        k_energy_bulk<float, 4><<<dim3(P->nbx, P->B), 288, eb_smem_bytes<float, 4>(P->eb_ns), P->stream>>>(
+            ea, fz, P->eb_H, P->eb_ns);
     else
         k_energy<T, SRC_INPLACE><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea, fz);
     stamp(P, 90);
@@ -611,6 +621,33 @@ cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full) {
     return persist_launch_v<T, MODE_MEAN, PREC_EXACT>(P, has_ref, full);
 }
 
+// k_energy_bulk geometry: band height H (halved until the items fill the
+// resident CTAs); returns CTAs per image
+template <typename T, int PX>
+int energy_bulk_occ(int ns) {
+    const size_t sm = eb_smem_bytes<T, PX>(ns);
+    cudaFuncSetAttribute(k_energy_bulk<T, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int bps = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_energy_bulk<T, PX>, 288, sm);
+    return std::max(1, bps);
+}
+template <typename T>
+int energy_bulk_cfg_impl(int batch, int m, int n, int px, int ns, int* H_out) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int bps = 1;
+    if (px == 1) bps = energy_bulk_occ<T, 1>(ns);
+    if (px == 2) bps = energy_bulk_occ<T, 2>(ns);
+    if (px == 4) bps = energy_bulk_occ<float, 4>(ns);
+    const long long per_img = std::max(1LL, (long long)nsm * bps / batch);
+    const long long ncb = (n + 256 * px - 1) / (256 * px);
+    int H = 32;
+    while (H > 2 && ((m + H - 1) / H) * ncb < per_img) H /= 2;
+    *H_out = H;
+    return (int)std::max(1LL, std::min(per_img, ((m + H - 1) / H) * ncb));
+}
+
 }  // namespace cmg
 
 #define CMG_INSTANTIATE(T)                                                          \
@@ -627,4 +664,8 @@ cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full) {
     template <>                                                                     \
     int cmg::coarse_region<T>(int layer) {                                          \
         return cmg::coarse_region_impl<T>(layer);                                   \
+    }                                                                               \
+    template <>                                                                     \
+    int cmg::energy_bulk_cfg<T>(int batch, int m, int n, int px, int ns, int* H) {  \
+        return cmg::energy_bulk_cfg_impl<T>(batch, m, n, px, ns, H);                \
     }

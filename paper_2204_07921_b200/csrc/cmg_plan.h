@@ -34,6 +34,7 @@ struct cmg_plan {
     cmg::Level lv[7];
     double* partials = nullptr;
     int nbx = 1;
+    int eb_px = 0, eb_ns = 4, eb_H = 32;  // k_energy_bulk<T, eb_px> (0: off)
     cmg::ImgState* st = nullptr;
     int* ndone = nullptr;
     int* iters = nullptr;
@@ -66,6 +67,7 @@ struct cmg_plan {
     int gkey = -1;
     bool use_while = true;
     int nodes_per_cycle = 0;
+    bool no_graph = false;  // CMG_NO_GRAPH=1: no graph at all (kernels visible to ncu)
     // stats
     long long launches = 0;
     int cycles_run = 0;
@@ -118,6 +120,8 @@ template <typename T>
 void enqueue_body_fused(cmg_plan* P, int full, bool has_ref);
 template <typename T>
 int coarse_region(int layer);
+template <typename T>
+int energy_bulk_cfg(int batch, int m, int n, int px, int ns, int* H);
 template <typename T>
 void enqueue_coop(cmg_plan* P, void* u, const int* seq, int nseq);
 bool make_tmap(CUtensorMap* out, const void* base, int esz, int m, int n, int B, int box);

@@ -27,7 +27,10 @@ VARIANTS = {
     "per_colour_only": {"CMG_FUSED": "0"},
     "persistent_kernel": {"CMG_FUSED": "0", "CMG_PERSIST": "1"},
     "host_chunked_graph": {"CMG_NO_WHILE": "1"},
+    "plain_stream_launches": {"CMG_NO_GRAPH": "1"},
     "separate_finalize": {"CMG_FUSED_FINALIZE": "0"},
+    "energy_bulk_copies": {"CMG_EBULK": "1"},
+    "energy_bulk_copies_2_stages": {"CMG_EBULK": "1", "CMG_EBULK_NS": "2"},
     "team_sizes_8_32": {"CMG_FUSE_MASK": "1", "CMG_TS2": "8", "CMG_TS3": "32"},
 }
 
