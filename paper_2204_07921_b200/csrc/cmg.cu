@@ -438,7 +438,16 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
         };
         P->fuse_mask = 1;
         if (layers >= 2 && tiles(3, tp2) >= 400 && tiles(3, tp2) * batch >= 2048) P->fuse_mask |= 2;
-        if (layers >= 3 && tiles(7, tp3) >= 400 && tiles(7, tp3) * batch >= 8192) P->fuse_mask |= 4;
+        // level 3: the per-colour team kernels beat the fused tile at every size
+        // measured (16384^2 fp32: 1.80 vs 2.92 ms; the tile recomputes ~2x the
+        // patches and holds 84 KB of shared memory per CTA), so it stays opt-in
+        (void)tp3;
+        // large fp32 fast jobs are throughput-bound: 8-lane teams (16384^2: 1.80
+        // vs 2.26 ms); small ones latency-bound, and fp64 exact prefers 16 lanes
+        // at every size (2048^2: 96 vs 266 us)
+        if (dtype == CMG_F32 && P->prec == CMG_PREC_FAST && (long long)batch * m * n >= (4LL << 20) &&
+            !getenv("CMG_TS3"))
+            P->ts3 = 8;
     }
     if (const char* fm = getenv("CMG_FUSE_MASK")) P->fuse_mask = atoi(fm) | 1;
     if (const char* dg = getenv("CMG_DBG")) P->dbg = atoi(dg);

@@ -13,4 +13,5 @@ p = N.Plan(m, n, B, 3, "mean", dt, "fast" if dt == "float32" else "exact")
 u = np.random.default_rng(0).random((B, m, n)).astype(dt)
 for i in range(4):
     assert N.lib().cmg_buffer_upload(p.handle, i, N.ptr(u)) == 0
+prime(p, B)
 print("energy us", p.time_sweep(0, -1, reps=reps) * 1e3)
