@@ -47,55 +47,84 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled (NVML, every 5 ms) during the timed
+    region; falls back to nvidia-smi when NVML is unavailable."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.reasons = set()
+        self.smax = None
+        self.stop_ev = threading.Event()
+        self.nvml = None
+
+    def _sample(self):
+        nv = self.nvml
+        self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+        mask = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+        for nm, bit in self.REASONS.items():
+            if mask & bit:
+                self.reasons.add(nm)
+
+    def _loop(self):
+        while not self.stop_ev.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nvml = nv
+            self.h = None
+            try:  # NVML ignores CUDA_VISIBLE_DEVICES: find the CUDA device by PCI address
+                import torch
+
+                pr = torch.cuda.get_device_properties(self.gpu)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self.h = nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                self.h = None
+            if self.h is None:
+                self.h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
-
-    def _read(self):
-        for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.nvml = None
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
+        if self.nvml is None:
+            return self._smi_once()
         try:
-            self.proc.wait(timeout=5)
+            self._sample()  # at least one sample, taken at the end of the timed region
         except Exception:
-            self.proc.kill()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+            pass
+        self.stop_ev.set()
+        self.t.join(timeout=1)
+        sm = self.samples
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml 5 ms"}
+
+    def _smi_once(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+            "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                 capture_output=True, text=True, timeout=10).stdout.strip()
+            parts = [x.strip() for x in out.split(",")]
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            reasons = [nm for nm, v in zip(names, parts[2:6]) if v.lower().startswith("active")]
+            return {"sm_mhz": float(parts[0]), "sm_max_mhz": float(parts[1]), "reasons": reasons, "samples": 1,
+                    "source": "nvidia-smi after the timed region"}
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock query unavailable"], "samples": 0}
 
 
 def dist_env():
@@ -368,6 +397,8 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": int(alg_bytes), "launch_ms": l1_ms, "peak_source": peak_src},
         "clocks": clocks,
     }
+    if rank == 0 and ws == 1 and not args.no_fine and args.config != 5:
+        line["roofline_fine_level"] = fine_level_roofline(local, peak)
     if cpu:
         line["cpu_baseline"] = cpu
     if rank == 0:
@@ -376,6 +407,42 @@ def run_ours(args):
         plan.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def fine_level_roofline(local: int, peak: float) -> dict:
+    """Level-1 sweep (the fine-level relaxation: all four colours, one launch)
+    at config 5's size, 16384^2 fp32 fast: 3 GiB of u/f, far beyond L2, so the
+    sweep streams HBM.  Algorithmic bytes = 12 per pixel (read u, read f,
+    write u).  Timed with CUDA events on the plan's stream (cmg_time_sweep)."""
+    import torch
+    from paper_2204_07921_b200 import _native as N
+    from paper_2204_07921_b200.strips import _DevView
+
+    size = 16384
+    p = N.Plan(size, size, 1, 3, "mean", "float32", "fast", device=local)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    src = torch.rand((size, size), device="cuda", dtype=torch.float32, generator=g)
+    for i in range(4):
+        ptr = ctypes.c_void_p()
+        assert N.lib().cmg_plan_buffer(p.handle, i, ctypes.byref(ptr)) == 0
+        torch.as_tensor(_DevView(ptr.value, (size, size), "<f4"), device="cuda").copy_(src)
+    del src
+    torch.cuda.synchronize()
+    en = np.zeros(2)
+    its = np.zeros(1, dtype=np.int32)
+    sts = np.zeros(1, dtype=np.int32)
+    rc = N.lib().cmg_solve_device(p.handle, None, None, None, 0.06, 1e-300, 1, 1, 0, 0, 1.0, N.dptr(en), None, None,
+                                  None, None, N.iptr(its), N.iptr(sts))
+    assert rc in (0, 2), N.last_error()
+    p.time_sweep(1, -1, reps=20)  # warm
+    ms = p.time_sweep(1, -1, reps=50)
+    p.close()
+    alg = 12 * size * size
+    ach = alg / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "kernel": "k_l1_x2 (level-1 sweep, four colours, fp32 fast, packed f32x2)",
+            "workload": "16384^2 fp32 (config 5 size), image far larger than L2",
+            "algorithmic_bytes_per_launch": alg, "launch_ms": ms}
 
 
 def run_strips(args, c, layers, dt, ws, rank, local, l2_flush, barrier, max_over_ranks):
@@ -452,6 +519,7 @@ def main():
     ap.add_argument("--dtype", choices=["float64", "float32"], default=None)
     ap.add_argument("--precision", choices=["exact", "fast"], default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fine", action="store_true", help="skip the 16384^2 fine-level roofline leg")
     args = ap.parse_args()
     if args.dtype is None:
         args.dtype = "float32" if args.config in (4, 5) else "float64"

@@ -55,6 +55,8 @@ struct FusedArgs {
     int m, n, mj, nj;
     int tiles_c;  // tiles per row of the tile grid
     int hc[4], wc[4];
+    int dbg;      // CMG_DBG bits (experiments)
+    float nz;     // -0.0f, opaque to the compiler (k_l1_x2 products)
     const SolveParams* P;
     ImgState* st;
 };

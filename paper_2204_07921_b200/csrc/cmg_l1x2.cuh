@@ -37,9 +37,14 @@ __device__ __forceinline__ F2 operator-(F2 a, F2 b) {
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
     return r;
 }
-__device__ __forceinline__ F2 operator*(F2 a, F2 b) {
+// Products are fma(a, b, nz) with nz = -0.0 held in a register loaded from a
+// kernel argument: bitwise the rounded product, but ptxas can neither fold it
+// to a multiply nor contract it with a neighbouring add.  (It does contract
+// mul.rn.f32x2 + add.rn.f32x2, differently per call site, which made two code
+// paths of the same formula differ by 1 ulp.)
+__device__ __forceinline__ F2 mul2(F2 a, F2 b, F2 nz) {
     F2 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(nz.v));
     return r;
 }
 __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
@@ -64,15 +69,15 @@ __device__ __forceinline__ F2 rsqrt2(F2 a) {
 }
 // reciprocal square root of a pair on the FMA pipe: bit-trick seed + 3 Newton
 // steps in packed fp32 (relative error ~1e-7), used to balance the MUFU pipe
-__device__ __forceinline__ F2 rsqrt2_nr(F2 a) {
+__device__ __forceinline__ F2 rsqrt2_nr(F2 a, F2 nz) {
     F2 y;
     asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\tshr.u32 lo, lo, 1;\n\tshr.u32 hi, hi, 1;\n\t"
         "sub.u32 lo, 0x5f375a86, lo;\n\tsub.u32 hi, 0x5f375a86, hi;\n\tmov.b64 %0, {lo, hi};\n\t}"
         : "=l"(y.v)
         : "l"(a.v));
-    const F2 mh = f2_splat(-0.5f) * a, c15 = f2_splat(1.5f);
+    const F2 mh = mul2(f2_splat(-0.5f), a, nz), c15 = f2_splat(1.5f);
 #pragma unroll
-    for (int it = 0; it < 3; ++it) y = y * fma2(mh, y * y, c15);
+    for (int it = 0; it < 3; ++it) y = mul2(y, fma2(mh, mul2(y, y, nz), c15), nz);
     return y;
 }
 __device__ __forceinline__ F2 lds2(const float* p) {
@@ -84,7 +89,7 @@ __device__ __forceinline__ F2 lds2(const float* p) {
 // closed-form level-1 c_half for two pixels (l1_chalf_fast, packed); NR > 0
 // moves the diagonal pairs' rsqrt to the FMA pipe (balances MUFU)
 template <int NR>
-__device__ __forceinline__ F2 l1_chalf_x2(F2 c, F2 E, F2 W, F2 N, F2 S, F2 NE, F2 NW, F2 SE, F2 SW) {
+__device__ __forceinline__ F2 l1_chalf_x2(F2 c, F2 E, F2 W, F2 N, F2 S, F2 NE, F2 NW, F2 SE, F2 SW, F2 nz) {
     const F2 m2 = f2_splat(-2.f);
     const F2 four = f2_splat(4.f), eight = f2_splat(8.f);
     auto pair = [&](F2 up, F2 um, F2 uq, F2 umq, F2 fourL, auto nr) {
@@ -94,9 +99,9 @@ __device__ __forceinline__ F2 l1_chalf_x2(F2 c, F2 E, F2 W, F2 N, F2 S, F2 NE, F
         const F2 base = fma2(D, D, fourL);
         const F2 Sa = fma2(m2, uq, sp), Sb = fma2(m2, umq, sp);
         if constexpr (decltype(nr)::value)
-            return Nn * (rsqrt2_nr(fma2(Sa, Sa, base)) + rsqrt2_nr(fma2(Sb, Sb, base)));
+            return mul2(Nn, rsqrt2_nr(fma2(Sa, Sa, base), nz) + rsqrt2_nr(fma2(Sb, Sb, base), nz), nz);
         else
-            return Nn * (rsqrt2(fma2(Sa, Sa, base)) + rsqrt2(fma2(Sb, Sb, base)));
+            return mul2(Nn, rsqrt2(fma2(Sa, Sa, base)) + rsqrt2(fma2(Sb, Sb, base)), nz);
     };
     using NO = std::integral_constant<bool, false>;
     using YES = std::integral_constant<bool, (NR > 0)>;
@@ -104,16 +109,16 @@ __device__ __forceinline__ F2 l1_chalf_x2(F2 c, F2 E, F2 W, F2 N, F2 S, F2 NE, F
     const F2 t2 = pair(N, S, W, E, four, NO{});
     const F2 t3 = pair(NE, SW, NW, SE, eight, YES{});
     const F2 t4 = pair(NW, SE, SW, NE, eight, NO{});
-    return fma2(f2_splat(1.41421356237309505f), t3 + t4, t1 + t2) * f2_splat(0.125f);
+    return mul2(fma2(f2_splat(1.41421356237309505f), t3 + t4, t1 + t2), f2_splat(0.125f), nz);
 }
 
-template <int TH, int TW, int NR>
-__global__ void __launch_bounds__(256) k_l1_x2(FusedArgs<float> a) {
+template <int TH, int TW, int NR, bool FAST = true, int NT = 256>
+__global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     using G = L1Geom<float, TH, TW>;
     static_assert(G::QW % 2 == 0, "pairs must stay 8-byte aligned");
     constexpr int PAIRS = G::QW / 2;             // packed pairs per plane row
-    constexpr int ROWS_PER_PASS = 256 / PAIRS;   // plane rows handled per pass
-    static_assert(256 % PAIRS == 0, "");
+    constexpr int ROWS_PER_PASS = NT / PAIRS;    // plane rows handled per pass
+    static_assert(NT % PAIRS == 0, "");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* su = reinterpret_cast<float*>(smem_raw) + 2;  // 2 guard words: p[-1] at the first pair stays in bounds
     float* sf = su + 4 * G::PLANE;
@@ -135,17 +140,32 @@ __global__ void __launch_bounds__(256) k_l1_x2(FusedArgs<float> a) {
     const bool vec = !border && (n % 4 == 0);
     if (vec) {
         // 16-byte loads: 4 consecutive pixels -> two 8-byte pairs of the two column planes
+        // all of a thread's 16-byte loads are issued before any is stored (NV4 x 2 in flight)
         constexpr int V4 = G::RW / 4;
-        for (int e = threadIdx.x; e < G::RH * V4; e += blockDim.x) {
+        constexpr int NV4 = (G::RH * V4 + NT - 1) / NT;
+        const float* ub = uin + (long long)r0 * n + c0;
+        const float* fbase = f + (long long)r0 * n + c0;
+        float4 uv[NV4], fv4[NV4];
+#pragma unroll
+        for (int j = 0; j < NV4; ++j) {
+            const int e = threadIdx.x + NT * j;
             const int i = e / V4, k = 4 * (e % V4);
-            const long long g = (long long)(r0 + i) * n + (c0 + k);
-            const float4 uv = *reinterpret_cast<const float4*>(uin + g);
-            const float4 fv4 = *reinterpret_cast<const float4*>(f + g);
-            const int p0 = G::idx(i, k), p1 = G::idx(i, k + 1);  // planes (i&1,0) and (i&1,1), word k/2
-            *reinterpret_cast<unsigned long long*>(su + p0) = f2_pack(uv.x, uv.z).v;
-            *reinterpret_cast<unsigned long long*>(su + p1) = f2_pack(uv.y, uv.w).v;
-            *reinterpret_cast<unsigned long long*>(sf + p0) = f2_pack(fv4.x, fv4.z).v;
-            *reinterpret_cast<unsigned long long*>(sf + p1) = f2_pack(fv4.y, fv4.w).v;
+            if (e < G::RH * V4) {
+                uv[j] = __ldg(reinterpret_cast<const float4*>(ub + (long long)i * n + k));
+                fv4[j] = __ldg(reinterpret_cast<const float4*>(fbase + (long long)i * n + k));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NV4; ++j) {
+            const int e = threadIdx.x + NT * j;
+            const int i = e / V4, k = 4 * (e % V4);
+            if (e < G::RH * V4) {
+                const int p0 = G::idx(i, k), p1 = G::idx(i, k + 1);  // planes (i&1,0) and (i&1,1), word k/2
+                *reinterpret_cast<unsigned long long*>(su + p0) = f2_pack(uv[j].x, uv[j].z).v;
+                *reinterpret_cast<unsigned long long*>(su + p1) = f2_pack(uv[j].y, uv[j].w).v;
+                *reinterpret_cast<unsigned long long*>(sf + p0) = f2_pack(fv4[j].x, fv4[j].z).v;
+                *reinterpret_cast<unsigned long long*>(sf + p1) = f2_pack(fv4[j].y, fv4[j].w).v;
+            }
         }
     } else {
         for (int e = threadIdx.x; e < G::RH * G::RW; e += blockDim.x) {
@@ -162,9 +182,81 @@ __global__ void __launch_bounds__(256) k_l1_x2(FusedArgs<float> a) {
     if (border) l1_reflect_fix<float, TH, TW>(su, r0, c0, m, n);
     const F2 w2 = f2_splat((float)a.P->w[1][0]);
     const F2 inv2 = f2_splat((float)(1.0 / a.P->den[1][0]));
+    const F2 nz2 = f2_splat(a.nz);  // -0.0f (see mul2)
     F2 finite_acc = f2_splat(0.f);  // stays 0 unless a correction is inf/NaN (x*0)
     const F2 zero2 = f2_splat(0.f);
     const int prow = threadIdx.x / PAIRS, pj = threadIdx.x % PAIRS;
+    if (!border && FAST) {
+        // Interior tile: a thread owns pair column pj and plane rows prow + k*ROWS_PER_PASS in every
+        // phase, so all neighbour addresses are one base register + a compile-time offset and the only
+        // per-pair bookkeeping is the phase's row / column range.
+        constexpr int ITERS = (G::QH + ROWS_PER_PASS - 1) / ROWS_PER_PASS;
+        const float* sb = su + prow * G::QW + 2 * pj;
+        float* sbw = su + prow * G::QW + 2 * pj;
+        const float* fb = sf + prow * G::QW + 2 * pj;
+        static_for<0, 4>([&](auto cphase) {
+            constexpr int c = decltype(cphase)::value;
+            constexpr int P = c >> 1, Q = c & 1;
+            constexpr int h = 3 - c;
+            constexpr int i_min = G::HALO - h, i_max = G::HALO + TH + h;
+            constexpr int k_min = G::HALO - h, k_max = G::HALO + TW + h;
+            constexpr int qi_lo = (i_min - P + 1) / 2, qi_hi = (i_max - P + 1) / 2;
+            constexpr int PL_c = (P * 2 + Q) * G::PLANE;
+            constexpr int PL_ns = ((1 - P) * 2 + Q) * G::PLANE;
+            constexpr int PL_ew = (P * 2 + (1 - Q)) * G::PLANE;
+            constexpr int PL_d = ((1 - P) * 2 + (1 - Q)) * G::PLANE;
+            constexpr int aN = (P - 1) >> 1, aS = (P + 1) >> 1;
+            constexpr int bE = (Q + 1) >> 1;
+            const int kA = 4 * pj + Q;
+            const bool okA = kA >= k_min && kA < k_max, okB = kA + 2 >= k_min && kA + 2 < k_max;
+            static_for<0, ITERS>([&](auto itc) {
+                constexpr int it = decltype(itc)::value;
+                constexpr int OFF = it * ROWS_PER_PASS * G::QW;
+                const int qi = prow + it * ROWS_PER_PASS;
+                if (qi >= qi_lo && qi < qi_hi && (okA || okB)) {
+                    auto pairEW = [&](auto rowoff, auto plane, F2& Ev, F2& Wv) {
+                        const float* p = sb + (decltype(plane)::value + OFF + decltype(rowoff)::value * G::QW);
+                        const F2 al = lds2(p);
+                        float lo, hi;
+                        f2_unpack(al, lo, hi);
+                        if constexpr (bE == 0) {
+                            Ev = al;
+                            Wv = f2_pack(p[-1], lo);
+                        } else {
+                            Wv = al;
+                            Ev = f2_pack(hi, p[2]);
+                        }
+                    };
+                    using IC0 = std::integral_constant<int, 0>;
+                    using ICN = std::integral_constant<int, aN>;
+                    using ICS = std::integral_constant<int, aS>;
+                    using ICEW = std::integral_constant<int, PL_ew>;
+                    using ICD = std::integral_constant<int, PL_d>;
+                    const F2 cv = lds2(sb + (PL_c + OFF));
+                    const F2 fv = lds2(fb + (PL_c + OFF));
+                    const F2 Nv = lds2(sb + (PL_ns + OFF + aN * G::QW));
+                    const F2 Sv = lds2(sb + (PL_ns + OFF + aS * G::QW));
+                    F2 Ev, Wv, NEv, NWv, SEv, SWv;
+                    pairEW(IC0{}, ICEW{}, Ev, Wv);
+                    pairEW(ICN{}, ICD{}, NEv, NWv);
+                    pairEW(ICS{}, ICD{}, SEv, SWv);
+                    const F2 ch = l1_chalf_x2<NR>(cv, Ev, Wv, Nv, Sv, NEv, NWv, SEv, SWv, nz2);
+                    const F2 corr = mul2(fma2(w2, fv - cv, ch), inv2, nz2);
+                    F2 nu = cv + corr;
+                    if (!(okA && okB)) {
+                        float c0v, c1v, n0, n1;
+                        f2_unpack(cv, c0v, c1v);
+                        f2_unpack(nu, n0, n1);
+                        nu = f2_pack(okA ? n0 : c0v, okB ? n1 : c1v);
+                    }
+                    *reinterpret_cast<unsigned long long*>(sbw + (PL_c + OFF)) = nu.v;
+                }
+            });
+            __syncthreads();
+        });
+        // non-finite corrections: every pixel's final value is computed identically by the tile
+        // that owns it, and a non-finite correction leaves a non-finite value -> check the outputs
+    } else
     static_for<0, 4>([&](auto cphase) {
         constexpr int c = decltype(cphase)::value;
         constexpr int P = c >> 1, Q = c & 1;
@@ -205,8 +297,8 @@ __global__ void __launch_bounds__(256) k_l1_x2(FusedArgs<float> a) {
             pairEW(0, PL_ew, Ev, Wv);
             pairEW(aN, PL_d, NEv, NWv);
             pairEW(aS, PL_d, SEv, SWv);
-            const F2 ch = l1_chalf_x2<NR>(cv, Ev, Wv, Nv, Sv, NEv, NWv, SEv, SWv);
-            const F2 corr = fma2(w2, fv - cv, ch) * inv2;  // (c_half + w f*) / (2 + w), f* = f - u
+            const F2 ch = l1_chalf_x2<NR>(cv, Ev, Wv, Nv, Sv, NEv, NWv, SEv, SWv, nz2);
+            const F2 corr = mul2(fma2(w2, fv - cv, ch), inv2, nz2);  // (c_half + w f*) / (2 + w), f* = f - u
             F2 nu = cv + corr;
             float c0v, c1v, n0, n1, k0, k1;
             f2_unpack(cv, c0v, c1v);
@@ -229,28 +321,34 @@ __global__ void __launch_bounds__(256) k_l1_x2(FusedArgs<float> a) {
         __syncthreads();
         if (border) l1_reflect_fix<float, TH, TW>(su, r0, c0, m, n);
     });
-    float fa0, fa1;
-    f2_unpack(finite_acc, fa0, fa1);
-    const bool bad = !(isfinite(fa0) && isfinite(fa1));
-    if (__syncthreads_or(bad) && threadIdx.x == 0) a.st[b].bad = 1;
     const bool vec_out = (R + TH <= m) && (C + TW <= n) && (n % 4 == 0);
     if (vec_out) {
         constexpr int V4 = TW / 4;
         for (int e = threadIdx.x; e < TH * V4; e += blockDim.x) {
             const int i = e / V4, k = 4 * (e % V4);
             const int p0 = G::idx(i + G::HALO, k + G::HALO), p1 = G::idx(i + G::HALO, k + G::HALO + 1);
+            const F2 v02 = lds2(su + p0), v13 = lds2(su + p1);
+            if (!border && FAST) finite_acc = fma2(v13, zero2, fma2(v02, zero2, finite_acc));
             float x0, x2, x1, x3;
-            f2_unpack(lds2(su + p0), x0, x2);
-            f2_unpack(lds2(su + p1), x1, x3);
+            f2_unpack(v02, x0, x2);
+            f2_unpack(v13, x1, x3);
             *reinterpret_cast<float4*>(uout + (long long)(R + i) * n + (C + k)) = make_float4(x0, x1, x2, x3);
         }
     } else {
         for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
             const int i = e / TW, k = e % TW;
             const int gi = R + i, gk = C + k;
-            if (gi < m && gk < n) uout[(long long)gi * n + gk] = su[G::idx(i + G::HALO, k + G::HALO)];
+            if (gi < m && gk < n) {
+                const float v = su[G::idx(i + G::HALO, k + G::HALO)];
+                if (!border && FAST) finite_acc = fma2(f2_pack(v, 0.f), zero2, finite_acc);
+                uout[(long long)gi * n + gk] = v;
+            }
         }
     }
+    float fa0, fa1;
+    f2_unpack(finite_acc, fa0, fa1);
+    const bool bad = !(isfinite(fa0) && isfinite(fa1));
+    if (__syncthreads_or(bad) && threadIdx.x == 0) a.st[b].bad = 1;
 }
 
 }  // namespace cmg

@@ -291,13 +291,29 @@ template <typename T, int MODE, int PREC>
 void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
     if constexpr (std::is_same<T, float>::value && MODE == MODE_MEAN && PREC == PREC_FAST) {
         if (P->l1x2) {  // packed fp32x2 variant
-            constexpr int TH = 56, TW = 56;
-            using G = L1Geom<float, TH, TW>;
-            const size_t smem = sizeof(float) * (2 + 8 * G::PLANE);
-            auto kern = P->l1x2 == 2 ? k_l1_x2<TH, TW, 1> : k_l1_x2<TH, TW, 0>;
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
-            kern<<<grd, 256, smem, P->stream>>>(a);
+            auto go = [&](auto kern, auto th, auto tw, int nt) {
+                constexpr int TH = decltype(th)::value, TW = decltype(tw)::value;
+                using G = L1Geom<float, TH, TW>;
+                const size_t smem = sizeof(float) * (2 + 8 * G::PLANE);
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
+                kern<<<grd, nt, smem, P->stream>>>(a);
+            };
+            using I56 = std::integral_constant<int, 56>;
+            using I120 = std::integral_constant<int, 120>;
+            using I88 = std::integral_constant<int, 88>;
+            // 1: interior fast path (default), 2: Newton rsqrt on the diagonals, 3: generic loop only,
+            // 4: 56 x 120 tiles, 5: 88 x 88 tiles (192 threads)
+            switch (P->l1x2) {
+                case 2: go(k_l1_x2<56, 56, 1>, I56{}, I56{}, 256); break;
+                case 3: go(k_l1_x2<56, 56, 0, false>, I56{}, I56{}, 256); break;
+                case 4: go(k_l1_x2<56, 120, 0>, I56{}, I120{}, 256); break;
+                case 5: go(k_l1_x2<88, 88, 0, true, 192>, I88{}, I88{}, 192); break;
+                case 6: go(k_l1_x2<56, 120, 0, false>, I56{}, I120{}, 256); break;
+                case 7: go(k_l1_x2<56, 120, 0, true, 512>, I56{}, I120{}, 512); break;
+                case 8: go(k_l1_x2<120, 56, 0>, I120{}, I56{}, 256); break;
+                default: go(k_l1_x2<56, 56, 0>, I56{}, I56{}, 256); break;
+            }
             return;
         }
     }
@@ -412,6 +428,8 @@ void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
     a.mj = L.mj;
     a.nj = L.nj;
     a.tiles_c = 0;  // set per variant by launch_fused
+    a.dbg = P->dbg;
+    a.nz = -0.0f;
     for (int c = 0; c < 4; ++c) {
         const int p = c >> 1, q = c & 1;
         a.hc[c] = (L.mj - p + 1) / 2;

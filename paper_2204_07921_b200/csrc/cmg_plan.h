@@ -55,7 +55,7 @@ struct cmg_plan {
     unsigned long long* stamps = nullptr;  // CMG_STAMPS diagnostics buffer
     int stamps_cap = 0;
     bool l1_tile = true;
-    int l1x2 = 1;  // 1: packed fp32x2 level-1 kernel (fp32 fast mean); 2: + Newton rsqrt on one pair  // packed fp32x2 level-1 kernel for fp32 fast mean mode
+    int l1x2 = 1;  // packed fp32x2 level-1 kernel (fp32 fast mean); variants in launch_l1_tile
     int fcfg2 = 0, fcfg3 = 0;
     bool coarse_tile = true;  // k_coarse_tile for fused levels 2-3
     bool coop = false;        // cooperative kernel for runs of non-fused coarse levels

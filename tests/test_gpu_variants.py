@@ -13,6 +13,7 @@ import subprocess
 import sys
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -89,3 +90,56 @@ def test_variant_bitexact(name):
     assert out.returncode == 0, out.stderr[-3000:]
     bad = json.loads(out.stdout.strip().splitlines()[-1])
     assert bad == [], f"{name}: mismatching cases {bad}"
+
+
+SCRIPT32 = r"""
+import sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+import paper_2204_07921_b200 as cmg
+from paper_2204_07921_b200 import synth
+f, _ = synth.config_input(1)
+f = np.tile(f, (3, 3))[:704, :640]
+cfg = cmg.SolverConfig(mode="mean", layers=3, max_outer=5, epsilon=1e-300, dtype="float32", precision="fast")
+img, tr = cmg.denoise(cmg.Image(f, 1.0), cfg)
+np.save(%(out)r, img.data)
+"""
+
+# same kernels, different code paths / schedules: bit-identical images
+VARIANTS32_EXACT = {
+    "l1_generic_loop": {"CMG_L1X2": "3"},
+    "l1_tiles_56x120": {"CMG_L1X2": "4"},
+    "l1_tiles_120x56": {"CMG_L1X2": "8"},
+    "l1_tiles_88x88_192_threads": {"CMG_L1X2": "5"},
+    "energy_bulk_copies": {"CMG_EBULK": "1"},
+    "host_chunked_graph": {"CMG_NO_WHILE": "1"},
+}
+# other kernel families (fused coarse tiles, per-colour kernels) evaluate the
+# fp32 fast closed forms with different reduction orders: equal to fp32 rounding
+VARIANTS32_CLOSE = {
+    "fused_all": {"CMG_FUSE_MASK": "7"},
+    "per_colour_only": {"CMG_FUSED": "0"},
+}
+
+
+def _run32(env_extra, tmp_path, tag):
+    env = dict(os.environ)
+    env.update(env_extra)
+    out = tmp_path / f"{tag}.npy"
+    r = subprocess.run([sys.executable, "-c", SCRIPT32 % {"root": str(ROOT), "out": str(out)}], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return np.load(out)
+
+
+@pytest.mark.parametrize("name", sorted(VARIANTS32_EXACT))
+def test_fp32_variant_same_image(name, tmp_path):
+    """fp32 fast: these variants reproduce the default path's image bit for bit."""
+    assert np.array_equal(_run32(VARIANTS32_EXACT[name], tmp_path, name), _run32({}, tmp_path, "default"))
+
+
+@pytest.mark.parametrize("name", sorted(VARIANTS32_CLOSE))
+def test_fp32_variant_close_image(name, tmp_path):
+    a = _run32(VARIANTS32_CLOSE[name], tmp_path, name)
+    b = _run32({}, tmp_path, "default")
+    assert np.abs(a.astype(np.float64) - b).max() <= 1e-5
