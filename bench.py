@@ -393,7 +393,7 @@ def run_ours(args):
                 "path": "cmg_solve (C ABI) with pinned host buffers"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_level_fused<level 1> (all four colours in one launch)",
+                     "traffic": traffic, "kernel": l1_kernel_name(args.dtype, args.precision, m_loc, n),
                      "algorithmic_bytes_per_launch": int(alg_bytes), "launch_ms": l1_ms, "peak_source": peak_src},
         "clocks": clocks,
     }
@@ -407,6 +407,15 @@ def run_ours(args):
         plan.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def l1_kernel_name(dtype: str, prec: str, m: int, n: int) -> str:
+    """The level-1 kernel the plan dispatches (cmg.cu plan heuristics)."""
+    if dtype == "float32" and prec == "fast":
+        tile = "56, 120" if m * n >= (4 << 20) and n >= 240 else "56, 56"
+        return f"k_l1_x2<{tile}> (level-1 sweep, four colours in one launch, packed f32x2)"
+    t = "double" if dtype == "float64" else "float"
+    return f"k_l1_tile<{t}, {prec}> (level-1 sweep, four colours in one launch)"
 
 
 def fine_level_roofline(local: int, peak: float) -> dict:
@@ -439,8 +448,12 @@ def fine_level_roofline(local: int, peak: float) -> dict:
     p.close()
     alg = 12 * size * size
     ach = alg / (ms * 1e-3) / 1e9
-    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "kernel": "k_l1_x2 (level-1 sweep, four colours, fp32 fast, packed f32x2)",
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("config5_float32_fast_l1")
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+            "kernel": l1_kernel_name("float32", "fast", size, size),
             "workload": "16384^2 fp32 (config 5 size), image far larger than L2",
             "algorithmic_bytes_per_launch": alg, "launch_ms": ms}
 
