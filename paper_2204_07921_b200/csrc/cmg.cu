@@ -77,6 +77,7 @@ bool make_tmap(CUtensorMap* out, const void* base, int esz, int m, int n, int B,
 namespace {
 
 __global__ void k_cond(cudaGraphConditionalHandle h, const int* ndone, int B, int* iters) {
+    cmg::pdl_sync();
     *iters += 1;
     cudaGraphSetConditional(h, (*ndone < B) ? 1u : 0u);
 }
@@ -449,6 +450,16 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
             !getenv("CMG_TS3"))
             P->ts3 = 8;
     }
+    // levels 2-3 as two row-parity launches each (k_rowpair): half the launches and
+    // half the traffic of four colour launches; they join the fused X -> Y rotation
+    // measured (B200, round 1): a win for latency-bound jobs (1024^2 fp64 fast: 4.13 -> 3.80 ms
+    // per solve; exact: level 3 only), a loss for large throughput-bound jobs (16384^2 level 2:
+    // 3.6 vs 1.3 ms with the coarse tile), where the per-colour / tile kernels stay
+    const bool small_job = (long long)batch * m * n < (4LL << 20);
+    P->rowpair = small_job ? (precision == CMG_PREC_FAST && mode == CMG_MODE_MEAN ? 3 : 2) : 0;
+    if (const char* rp = getenv("CMG_ROWPAIR")) P->rowpair = atoi(rp) & 3;
+    if (layers >= 2 && (P->rowpair & 1)) P->fuse_mask |= 2;
+    if (layers >= 3 && (P->rowpair & 2)) P->fuse_mask |= 4;
     if (const char* fm = getenv("CMG_FUSE_MASK")) P->fuse_mask = atoi(fm) | 1;
     if (const char* dg = getenv("CMG_DBG")) P->dbg = atoi(dg);
     if (const char* sp = getenv("CMG_STAMPS")) {
@@ -547,6 +558,17 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     long long want = std::max(1, 1184 / batch);
     if (const char* nb = getenv("CMG_ENERGY_CTAS")) want = std::max(1, atoi(nb) / batch);
     P->nbx = (int)std::max(1LL, std::min(want, (long long)(m + 3) / 4));
+    if (const char* et = getenv("CMG_ENERGY_TARGET")) {
+        // opt-in 2-D grid (row bands x 256-column chunks, one column per thread).  Measured
+        // at 1024^2 (B200): 21 us at 256 CTAs, 28 us at 1024, 37 us at 2048 vs 19.8 us for
+        // the default 256 full-width bands -- the per-CTA ticket atomics and the longer
+        // finalize outweigh the shorter per-thread chains
+        P->ncb = (int)((n + 255) / 256);
+        const long long target = std::max(1, atoi(et));
+        const long long nrb = std::max(1LL, std::min<long long>((target + batch * P->ncb - 1) / (batch * P->ncb),
+                                                                (m + 1) / 2));
+        P->nbx = (int)(nrb * P->ncb);
+    }
     // rows streamed by bulk async copies (k_energy_bulk): 16-byte aligned rows
     {
         const char* eb = getenv("CMG_EBULK");
@@ -563,6 +585,7 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
             const int nb = dtype == CMG_F64 ? energy_bulk_cfg<double>(batch, m, n, P->eb_px, P->eb_ns, &P->eb_H)
                                             : energy_bulk_cfg<float>(batch, m, n, P->eb_px, P->eb_ns, &P->eb_H);
             if (!getenv("CMG_ENERGY_CTAS")) P->nbx = nb;
+            P->ncb = 1;
         }
     }
     if (getenv("CMG_VERBOSE"))
@@ -578,6 +601,7 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     CKP(cudaMalloc(&P->tickets, sizeof(int) * (batch + 1)));
     CKP(cudaMemset(P->tickets, 0, sizeof(int) * (batch + 1)));
     if (const char* ff = getenv("CMG_FUSED_FINALIZE")) P->fused_finalize = atoi(ff) != 0;
+    if (const char* pd = getenv("CMG_PDL")) P->pdl = atoi(pd) != 0;
     CKP(cudaMalloc(&P->P, sizeof(SolveParams)));
 #undef CKP
     *out = P;

@@ -332,6 +332,7 @@ __device__ __forceinline__ T coarse_solve_team(const T* su, const T* sf, int bas
 template <typename T, int LAYER, int MODE, int PREC, int TP, int TS, int NT>
 __global__ void __launch_bounds__(NT) k_coarse_tile(FusedArgs<T> a, const __grid_constant__ CUtensorMap tmu,
                                                     const __grid_constant__ CUtensorMap tmf, int use_tma) {
+    pdl_sync();
     using G = CoarseGeom<T, LAYER, TP>;
     constexpr int S = G::S, RD = G::RD, LD = G::LD;
     extern __shared__ __align__(128) unsigned char smem_raw[];

@@ -75,6 +75,7 @@ __device__ __forceinline__ void eb_lds(const T* p, T (&v)[PX]) {
 // stage's bytes have landed, empty[s] when all 8 consumer warps released it.
 template <typename T, int PX>
 __global__ void __launch_bounds__(288) k_energy_bulk(EnergyArgs a, EnergyFin fz, int H, int NS) {
+    pdl_sync();
     using G = EBGeom<T, PX>;
     using A = T;
     extern __shared__ __align__(128) unsigned char eb_smem[];

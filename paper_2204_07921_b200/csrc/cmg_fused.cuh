@@ -155,7 +155,8 @@ __device__ __noinline__ void fused_phases_border(T* su, T* sf, int ld, int r0, i
 }
 
 template <typename T, int LAYER, int MODE, int PREC, int TP, int TS>
-__global__ void __launch_bounds__(256) k_level_fused(FusedArgs<T> a) {  // blockDim <= 256
+__global__ void __launch_bounds__(256) k_level_fused(FusedArgs<T> a) {
+    pdl_sync();  // blockDim <= 256
     using G = FusedGeom<LAYER, TP>;
     constexpr int S = G::S, RD = G::RD;
     extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -85,8 +85,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Rare orderings, kept out of line so the hot kernels stay small (I-cache):
 // f* of a colour class with a single patch column (NumPy coalesces the patch
 // into one flat pairwise sum) ...
-template <typename T, int S, class Acc>
-__device__ __noinline__ T fstar_flat_sum(const Acc U, const Acc F, int R0, int C0) {
+template <typename T, int S, class Acc, class AccF = Acc>
+__device__ __noinline__ T fstar_flat_sum(const Acc U, const AccF F, int R0, int C0) {
     using O = X<T>;
     return O::add(T(0), pairwise_small<T>(S * S, [&](int e) {
         return O::sub(F(R0 + e / S, C0 + e % S), U(R0 + e / S, C0 + e % S));
@@ -220,6 +220,7 @@ __device__ __forceinline__ T patch_solve_ct_border(const T* u, const T* f, int R
 
 template <typename T, int LAYER, int MODE, int PREC, int SRC>
 __global__ void __launch_bounds__(256) k_sweep_tpp(SweepArgs<T> a) {
+    pdl_sync();
     const int b = blockIdx.z;
     if (a.st[b].done) return;
     const int pc = blockIdx.x * blockDim.x + threadIdx.x;
@@ -285,8 +286,8 @@ __device__ __forceinline__ ArgBest<T> arg_reduce(ArgBest<T> x) {
     return x;
 }
 
-template <typename T, int LAYER, int MODE, int PREC, int TS, class Acc>
-__device__ __forceinline__ T patch_solve_team(const Acc& U, const Acc& F, int R0, int C0, int lane,
+template <typename T, int LAYER, int MODE, int PREC, int TS, class Acc, class AccF = Acc>
+__device__ __forceinline__ T patch_solve_team(const Acc& U, const AccF& F, int R0, int C0, int lane,
                                               const SweepArgs<T>& a) {
     using O = X<T>;
     constexpr int S = (1 << LAYER) - 1;
@@ -393,15 +394,16 @@ __device__ __forceinline__ T patch_solve_team_border(const T* u, const T* f, int
 
 template <typename T, int LAYER, int MODE, int PREC, int SRC, int TS>
 __global__ void __launch_bounds__(256) k_sweep_team(SweepArgs<T> a) {
+    pdl_sync();
     const int b = blockIdx.z;
     if (a.st[b].done) return;  // uniform per block
     constexpr int S = (1 << LAYER) - 1;
     const int lane = threadIdx.x % TS;
-    const long long npatch = (long long)a.hc * a.wc;
-    long long idx = (long long)blockIdx.x * (blockDim.x / TS) + threadIdx.x / TS;
+    const int npatch = a.hc * a.wc;  // < 2^31 (m*n < 2^31)
+    int idx = (int)blockIdx.x * (256 / TS) + (int)threadIdx.x / TS;
     const bool valid = idx < npatch;
     if (!valid) idx = npatch - 1;  // keep the whole warp converged for the shuffles
-    const int pr = (int)(idx / a.wc), pc = (int)(idx % a.wc);
+    const int pr = idx / a.wc, pc = idx - pr * a.wc;
     const int R0 = (2 * pr + a.p) * S, C0 = (2 * pc + a.q) * S;
     T* u = a.u + (long long)b * a.istride;
     const T* f = a.f + (long long)b * a.istride;
@@ -503,6 +505,7 @@ __device__ __forceinline__ void bpp_body(const Acc& U, const Acc& F, int R0, int
 
 template <typename T, int MODE, int SRC>
 __global__ void __launch_bounds__(128) k_sweep_bpp(SweepArgs<T> a) {
+    pdl_sync();
     __shared__ T sh_rows[64];
     __shared__ T sh_vals[256];
     __shared__ T sh_c;
@@ -550,6 +553,7 @@ struct EnergyArgs {
     const void* upad;  // padded (pad 1) snapshot when SRC_PADDED
     long long istride, pstride;
     int m, n, W, mode, nbx;
+    int ncb;               // k_energy: column chunks per row band (nbx = row bands * ncb)
     long long e_lo, e_hi;  // pixel index range of the sums (whole image: 0..m*n)
     double* partials;      // [B][nbx][5]
     const ImgState* st;
@@ -598,6 +602,7 @@ __device__ __forceinline__ void finalize_image(int b, const double* partials, in
     const int tid = threadIdx.x;
     double acc[NSUM] = {0, 0, 0, 0, 0};
     if (tid < 256) {
+#pragma unroll 4
         for (int i = tid; i < nbx; i += 256)
 #pragma unroll
             for (int s = 0; s < NSUM; ++s) acc[s] += __ldcg(&partials[((long long)b * nbx + i) * NSUM + s]);
@@ -681,6 +686,7 @@ __device__ __forceinline__ void finalize_image(int b, const double* partials, in
 
 static __global__ void __launch_bounds__(256) k_finalize(const double* partials, int nbx, const SolveParams* P,
                                                          ImgState* st, TraceArgs tr, int initial) {
+    pdl_sync();
     finalize_image(blockIdx.x, partials, nbx, P, st, tr, initial);
 }
 
@@ -746,6 +752,7 @@ __device__ __forceinline__ void energy_reduce_finalize(const double (&acc)[NSUM]
 
 template <typename T, int SRC>
 __global__ void __launch_bounds__(256) k_energy(EnergyArgs a, EnergyFin fz) {
+    pdl_sync();
     using A = T;
     const int b = blockIdx.y;
     const int tid = threadIdx.x;
@@ -758,12 +765,16 @@ __global__ void __launch_bounds__(256) k_energy(EnergyArgs a, EnergyFin fz) {
         const T* rf = a.ref ? (const T*)a.ref + (long long)b * a.istride : nullptr;
         const int n = a.n, m = a.m;
         const int r_lo = (int)(a.e_lo / n), r_hi = (int)(a.e_hi / n);
-        // each CTA owns a band of rows; a thread walks down its columns keeping
-        // the 3x3 neighbourhood in registers (3 new u loads per pixel)
+        // each CTA owns a band of rows x a chunk of columns; a thread walks down
+        // its columns keeping the 3x3 neighbourhood in registers (3 new u loads
+        // per pixel).  Small images use many short bands (latency-bound pass).
         const int rows = r_hi - r_lo;
-        const int band = (rows + a.nbx - 1) / a.nbx;
-        const int i0 = r_lo + blockIdx.x * band, i1 = min(r_hi, i0 + band);
-        for (int k = tid; k < n && i0 < i1; k += blockDim.x) {
+        const int nrb = a.nbx / a.ncb, rb = blockIdx.x / a.ncb, cb = blockIdx.x % a.ncb;
+        const int band = (rows + nrb - 1) / nrb;
+        const int i0 = r_lo + rb * band, i1 = min(r_hi, i0 + band);
+        const int cw = (n + a.ncb - 1) / a.ncb;
+        const int k1 = min(n, (cb + 1) * cw);
+        for (int k = cb * cw + tid; k < k1 && i0 < i1; k += blockDim.x) {
             const bool kin = (k >= 1) && (k + 1 < n);
             auto ldrow = [&](int i, A& wv, A& cv, A& ev) {
                 if (SRC == SRC_PADDED) {
@@ -862,6 +873,7 @@ __device__ void reflect_line(T* line, long long stride, int left, int len, int r
 template <typename T>
 __global__ void k_pad_copy(const T* __restrict__ src, long long istride, T* dst, long long pstride, int m, int n,
                            int W, const ImgState* st) {
+    pdl_sync();
     const int b = blockIdx.y;
     if (st && st[b].done) return;
     const long long N = (long long)m * n;
@@ -875,6 +887,7 @@ __global__ void k_pad_copy(const T* __restrict__ src, long long istride, T* dst,
 template <typename T>
 __global__ void k_pad_axis(T* buf, long long pstride, int axis, int m, int n, int H, int W, int bot, int rgt,
                            const ImgState* st) {
+    pdl_sync();
     const int b = blockIdx.y;
     if (st && st[b].done) return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;

@@ -201,6 +201,7 @@ __device__ __forceinline__ void l1_reflect_fix(T* su, int r0, int c0, int m, int
 
 template <typename T, int MODE, int PREC, int TH, int TW>
 __global__ void __launch_bounds__(256) k_l1_tile(FusedArgs<T> a) {
+    pdl_sync();
     using G = L1Geom<T, TH, TW>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* su = reinterpret_cast<T*>(smem_raw);

@@ -114,6 +114,7 @@ __device__ __forceinline__ F2 l1_chalf_x2(F2 c, F2 E, F2 W, F2 N, F2 S, F2 NE, F
 
 template <int TH, int TW, int NR, bool FAST = true, int NT = 256>
 __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
+    pdl_sync();
     using G = L1Geom<float, TH, TW>;
     static_assert(G::QW % 2 == 0, "pairs must stay 8-byte aligned");
     constexpr int PAIRS = G::QW / 2;             // packed pairs per plane row
@@ -139,32 +140,47 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     const bool border = (r0 < 1) || (c0 < 1) || (r0 + G::RH >= m) || (c0 + G::RW >= n);
     const bool vec = !border && (n % 4 == 0);
     if (vec) {
-        // 16-byte loads: 4 consecutive pixels -> two 8-byte pairs of the two column planes
-        // all of a thread's 16-byte loads are issued before any is stored (NV4 x 2 in flight)
+        // 16-byte loads: 4 consecutive pixels -> two 8-byte pairs of the two column planes.
+        // Thread t owns float4 column c4 = t % V4 of region rows t / V4 + j * RSTEP: one 64-bit
+        // base pointer, constant row strides, a fixed row parity (RSTEP is even) and
+        // compile-time shared-memory offsets.
         constexpr int V4 = G::RW / 4;
-        constexpr int NV4 = (G::RH * V4 + NT - 1) / NT;
-        const float* ub = uin + (long long)r0 * n + c0;
-        const float* fbase = f + (long long)r0 * n + c0;
+        constexpr int RSTEP = NT / V4;
+        constexpr int NV4 = (G::RH + RSTEP - 1) / RSTEP;
+        static_assert(NT % V4 == 0 && RSTEP % 2 == 0, "staging map");
+        const int c4 = threadIdx.x % V4, row = threadIdx.x / V4;
+        const long long g0 = (long long)(r0 + row) * n + c0 + 4 * c4;
+        const float4* ub = reinterpret_cast<const float4*>(uin + g0);
+        const float4* fbp = reinterpret_cast<const float4*>(f + g0);
+        const int rstride4 = RSTEP * (n / 4);  // float4 per RSTEP image rows
+        {
+            // L2 prefetch of every 128-byte line of the region (u and f) first: the
+            // register-staged loads below then merge into requests already in flight
+            constexpr int LPR = G::RW / 32 + 1;  // lines per region row (c0 is not line aligned)
+            constexpr int NPF = 2 * G::RH * LPR;
+            for (int e = threadIdx.x; e < NPF && !(a.dbg & 0x10000); e += NT) {  // CMG_DBG bit 16: off
+                const int arr = e / (G::RH * LPR), rem = e % (G::RH * LPR);
+                const float* base = (arr ? f : uin) + (long long)(r0 + rem / LPR) * n + c0 + 32 * (rem % LPR);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(base));
+            }
+        }
         float4 uv[NV4], fv4[NV4];
 #pragma unroll
         for (int j = 0; j < NV4; ++j) {
-            const int e = threadIdx.x + NT * j;
-            const int i = e / V4, k = 4 * (e % V4);
-            if (e < G::RH * V4) {
-                uv[j] = __ldg(reinterpret_cast<const float4*>(ub + (long long)i * n + k));
-                fv4[j] = __ldg(reinterpret_cast<const float4*>(fbase + (long long)i * n + k));
+            if (G::RH % RSTEP == 0 || row + j * RSTEP < G::RH) {
+                uv[j] = __ldg(ub + j * rstride4);
+                fv4[j] = __ldg(fbp + j * rstride4);
             }
         }
+        const int s0 = (row & 1) * 2 * G::PLANE + (row >> 1) * G::QW + 2 * c4;  // plane (p,0), word 2*c4
 #pragma unroll
         for (int j = 0; j < NV4; ++j) {
-            const int e = threadIdx.x + NT * j;
-            const int i = e / V4, k = 4 * (e % V4);
-            if (e < G::RH * V4) {
-                const int p0 = G::idx(i, k), p1 = G::idx(i, k + 1);  // planes (i&1,0) and (i&1,1), word k/2
-                *reinterpret_cast<unsigned long long*>(su + p0) = f2_pack(uv[j].x, uv[j].z).v;
-                *reinterpret_cast<unsigned long long*>(su + p1) = f2_pack(uv[j].y, uv[j].w).v;
-                *reinterpret_cast<unsigned long long*>(sf + p0) = f2_pack(fv4[j].x, fv4[j].z).v;
-                *reinterpret_cast<unsigned long long*>(sf + p1) = f2_pack(fv4[j].y, fv4[j].w).v;
+            if (G::RH % RSTEP == 0 || row + j * RSTEP < G::RH) {
+                const int o = s0 + j * (RSTEP / 2) * G::QW;
+                *reinterpret_cast<unsigned long long*>(su + o) = f2_pack(uv[j].x, uv[j].z).v;
+                *reinterpret_cast<unsigned long long*>(su + o + G::PLANE) = f2_pack(uv[j].y, uv[j].w).v;
+                *reinterpret_cast<unsigned long long*>(sf + o) = f2_pack(fv4[j].x, fv4[j].z).v;
+                *reinterpret_cast<unsigned long long*>(sf + o + G::PLANE) = f2_pack(fv4[j].y, fv4[j].w).v;
             }
         }
     } else {
@@ -323,16 +339,30 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     });
     const bool vec_out = (R + TH <= m) && (C + TW <= n) && (n % 4 == 0);
     if (vec_out) {
-        constexpr int V4 = TW / 4;
-        for (int e = threadIdx.x; e < TH * V4; e += blockDim.x) {
-            const int i = e / V4, k = 4 * (e % V4);
-            const int p0 = G::idx(i + G::HALO, k + G::HALO), p1 = G::idx(i + G::HALO, k + G::HALO + 1);
-            const F2 v02 = lds2(su + p0), v13 = lds2(su + p1);
-            if (!border && FAST) finite_acc = fma2(v13, zero2, fma2(v02, zero2, finite_acc));
-            float x0, x2, x1, x3;
-            f2_unpack(v02, x0, x2);
-            f2_unpack(v13, x1, x3);
-            *reinterpret_cast<float4*>(uout + (long long)(R + i) * n + (C + k)) = make_float4(x0, x1, x2, x3);
+        // thread t writes float4 column c4 = t % CW (< TW/4) of tile rows t / CW + j * OSTEP
+        constexpr int TV4 = TW / 4;
+        constexpr int CW = TV4 <= 8 ? 8 : (TV4 <= 16 ? 16 : 32);
+        constexpr int OSTEP = NT / CW;
+        constexpr int NO = (TH + OSTEP - 1) / OSTEP;
+        static_assert(NT % CW == 0 && OSTEP % 2 == 0 && TV4 <= 32, "output map");
+        const int c4 = threadIdx.x % CW, row = threadIdx.x / CW;
+        if (c4 < TV4) {
+            float4* op = reinterpret_cast<float4*>(uout + (long long)(R + row) * n + C + 4 * c4);
+            const int ostride4 = OSTEP * (n / 4);
+            // region pixel (HALO + row, HALO + 4 c4): row parity fixed, even column -> word HALO/2 + 2 c4
+            const int s0 = ((G::HALO + row) & 1) * 2 * G::PLANE + ((G::HALO + row) >> 1) * G::QW + G::HALO / 2 + 2 * c4;
+#pragma unroll
+            for (int j = 0; j < NO; ++j) {
+                if (TH % OSTEP == 0 || row + j * OSTEP < TH) {
+                    const int o = s0 + j * (OSTEP / 2) * G::QW;
+                    const F2 v02 = lds2(su + o), v13 = lds2(su + o + G::PLANE);
+                    if (!border && FAST) finite_acc = fma2(v13, zero2, fma2(v02, zero2, finite_acc));
+                    float x0, x2, x1, x3;
+                    f2_unpack(v02, x0, x2);
+                    f2_unpack(v13, x1, x3);
+                    op[j * ostride4] = make_float4(x0, x1, x2, x3);
+                }
+            }
         }
     } else {
         for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {

@@ -13,6 +13,7 @@
 #include "cmg_coarse.cuh"
 #include "cmg_energy_bulk.cuh"
 #include "cmg_persist.cuh"
+#include "cmg_rowpair.cuh"
 #include "cmg_plan.h"
 
 namespace cmg {
@@ -22,66 +23,65 @@ void enqueue_pad(cmg_plan* P, const void* src, void* dst, int H, int W, long lon
                  bool gate) {
     const ImgState* st = gate ? P->st : nullptr;
     const int blocks = (int)std::min<long long>((P->N + 255) / 256, 4096);
-    k_pad_copy<T><<<dim3(blocks, P->B), 256, 0, P->stream>>>((const T*)src, P->N, (T*)dst, pstride, P->m, P->n, W,
+    klaunch(P, k_pad_copy<T>, dim3(blocks, P->B), 256, 0, (const T*)src, P->N, (T*)dst, pstride, P->m, P->n, W,
                                                              st);
-    k_pad_axis<T><<<dim3((P->n + 127) / 128, P->B), 128, 0, P->stream>>>((T*)dst, pstride, 0, P->m, P->n, H, W,
+    klaunch(P, k_pad_axis<T>, dim3((P->n + 127) / 128, P->B), 128, 0, (T*)dst, pstride, 0, P->m, P->n, H, W,
                                                                          bot, rgt, st);
-    k_pad_axis<T><<<dim3((H + 127) / 128, P->B), 128, 0, P->stream>>>((T*)dst, pstride, 1, P->m, P->n, H, W, bot,
+    klaunch(P, k_pad_axis<T>, dim3((H + 127) / 128, P->B), 128, 0, (T*)dst, pstride, 1, P->m, P->n, H, W, bot,
                                                                       rgt, st);
     P->enq += 3;
 }
 
 template <typename T, int LAYER, int MODE, int PREC>
-void launch_tpp(const SweepArgs<T>& a, bool padded, int B, cudaStream_t s) {
+void launch_tpp(const cmg_plan* P, const SweepArgs<T>& a, bool padded, int B) {
     const dim3 blk(32, 8);
     const dim3 grd((a.wc + 31) / 32, (a.hc + 7) / 8, B);
     if (padded)
-        k_sweep_tpp<T, LAYER, MODE, PREC, SRC_PADDED><<<grd, blk, 0, s>>>(a);
+        klaunch(P, k_sweep_tpp<T, LAYER, MODE, PREC, SRC_PADDED>, grd, blk, 0, a);
     else
-        k_sweep_tpp<T, LAYER, MODE, PREC, SRC_INPLACE><<<grd, blk, 0, s>>>(a);
+        klaunch(P, k_sweep_tpp<T, LAYER, MODE, PREC, SRC_INPLACE>, grd, blk, 0, a);
 }
 
 template <typename T, int LAYER, int MODE, int PREC, int TS>
-void launch_team(const SweepArgs<T>& a, bool padded, int B, cudaStream_t s) {
+void launch_team(const cmg_plan* P, const SweepArgs<T>& a, bool padded, int B) {
     const long long np = (long long)a.hc * a.wc;
     const int per_block = 256 / TS;
     const dim3 grd((unsigned)((np + per_block - 1) / per_block), 1, B);
     if (padded)
-        k_sweep_team<T, LAYER, MODE, PREC, SRC_PADDED, TS><<<grd, 256, 0, s>>>(a);
+        klaunch(P, k_sweep_team<T, LAYER, MODE, PREC, SRC_PADDED, TS>, grd, 256, 0, a);
     else
-        k_sweep_team<T, LAYER, MODE, PREC, SRC_INPLACE, TS><<<grd, 256, 0, s>>>(a);
+        klaunch(P, k_sweep_team<T, LAYER, MODE, PREC, SRC_INPLACE, TS>, grd, 256, 0, a);
 }
 
 template <typename T, int MODE, int PREC>
 void dispatch_small_layer(const cmg_plan* P, const SweepArgs<T>& a, bool padded) {
     switch (a.layer) {
-        case 1: launch_tpp<T, 1, MODE, PREC>(a, padded, P->B, P->stream); break;
+        case 1: launch_tpp<T, 1, MODE, PREC>(P, a, padded, P->B); break;
         case 2:
             if (P->ts2 == 16)
-                launch_team<T, 2, MODE, PREC, 16>(a, padded, P->B, P->stream);
+                launch_team<T, 2, MODE, PREC, 16>(P, a, padded, P->B);
             else if (P->ts2 == 8)
-                launch_team<T, 2, MODE, PREC, 8>(a, padded, P->B, P->stream);
+                launch_team<T, 2, MODE, PREC, 8>(P, a, padded, P->B);
             else
-                launch_team<T, 2, MODE, PREC, 4>(a, padded, P->B, P->stream);
+                launch_team<T, 2, MODE, PREC, 4>(P, a, padded, P->B);
             break;
         default:
             if (P->ts3 == 32)
-                launch_team<T, 3, MODE, PREC, 32>(a, padded, P->B, P->stream);
+                launch_team<T, 3, MODE, PREC, 32>(P, a, padded, P->B);
             else if (P->ts3 == 16)
-                launch_team<T, 3, MODE, PREC, 16>(a, padded, P->B, P->stream);
+                launch_team<T, 3, MODE, PREC, 16>(P, a, padded, P->B);
             else
-                launch_team<T, 3, MODE, PREC, 8>(a, padded, P->B, P->stream);
+                launch_team<T, 3, MODE, PREC, 8>(P, a, padded, P->B);
             break;
     }
 }
 
+// kernel arguments of one colour of a level (driver.sweep_layer, driver.py:225-251)
 template <typename T>
-void enqueue_sweep(cmg_plan* P, int layer, int color) {
-    Level& L = P->lv[layer];
+SweepArgs<T> make_sweep_args(const cmg_plan* P, int layer, int color) {
+    const Level& L = P->lv[layer];
     const int p = color >> 1, q = color & 1;
     const int hc = (L.mj - p + 1) / 2, wc = (L.nj - q + 1) / 2;
-    if (hc <= 0 || wc <= 0) return;
-    if (L.general) enqueue_pad<T>(P, P->u, P->upad, L.H, L.W, L.pstride, 1 + L.mp - P->m, 1 + L.np - P->n, true);
     SweepArgs<T> a;
     a.u = (T*)P->u;
     a.f = (const T*)P->f;
@@ -108,6 +108,17 @@ void enqueue_sweep(cmg_plan* P, int layer, int color) {
     a.bk.w0 = P->hostP.w[layer][0];
     a.bk.den0 = P->hostP.den[layer][0];
     a.bk.inv0 = 1.0 / P->hostP.den[layer][0];
+    return a;
+}
+
+template <typename T>
+void enqueue_sweep(cmg_plan* P, int layer, int color) {
+    Level& L = P->lv[layer];
+    const int p = color >> 1, q = color & 1;
+    const int hc = (L.mj - p + 1) / 2, wc = (L.nj - q + 1) / 2;
+    if (hc <= 0 || wc <= 0) return;
+    if (L.general) enqueue_pad<T>(P, P->u, P->upad, L.H, L.W, L.pstride, 1 + L.mp - P->m, 1 + L.np - P->n, true);
+    const SweepArgs<T> a = make_sweep_args<T>(P, layer, color);
     const bool padded = L.general;
     if (layer <= 3) {
         if (P->mode == CMG_MODE_GAUSS)
@@ -120,14 +131,14 @@ void enqueue_sweep(cmg_plan* P, int layer, int color) {
         const dim3 grd(wc, hc, P->B);
         if (P->mode == CMG_MODE_GAUSS) {
             if (padded)
-                k_sweep_bpp<T, MODE_GAUSS, SRC_PADDED><<<grd, 128, 0, P->stream>>>(a);
+                klaunch(P, k_sweep_bpp<T, MODE_GAUSS, SRC_PADDED>, grd, 128, 0, a);
             else
-                k_sweep_bpp<T, MODE_GAUSS, SRC_INPLACE><<<grd, 128, 0, P->stream>>>(a);
+                klaunch(P, k_sweep_bpp<T, MODE_GAUSS, SRC_INPLACE>, grd, 128, 0, a);
         } else {
             if (padded)
-                k_sweep_bpp<T, MODE_MEAN, SRC_PADDED><<<grd, 128, 0, P->stream>>>(a);
+                klaunch(P, k_sweep_bpp<T, MODE_MEAN, SRC_PADDED>, grd, 128, 0, a);
             else
-                k_sweep_bpp<T, MODE_MEAN, SRC_INPLACE><<<grd, 128, 0, P->stream>>>(a);
+                klaunch(P, k_sweep_bpp<T, MODE_MEAN, SRC_INPLACE>, grd, 128, 0, a);
         }
     }
     P->enq += 1;
@@ -136,6 +147,7 @@ void enqueue_sweep(cmg_plan* P, int layer, int color) {
 
 template <typename T>
 __global__ void k_copy(const T* __restrict__ src, T* __restrict__ dst, long long N, const ImgState* st) {
+    pdl_sync();
     const int b = blockIdx.y;
     if (st[b].done) return;
     const long long off = (long long)b * N;
@@ -146,7 +158,7 @@ __global__ void k_copy(const T* __restrict__ src, T* __restrict__ dst, long long
 template <typename T>
 void enqueue_copy_prev(cmg_plan* P) {
     const int blocks = (int)std::min<long long>((P->N + 255) / 256, 2048);
-    k_copy<T><<<dim3(blocks, P->B), 256, 0, P->stream>>>((const T*)P->u, (T*)P->uprev, P->N, P->st);
+    klaunch(P, k_copy<T>, dim3(blocks, P->B), 256, 0, (const T*)P->u, (T*)P->uprev, P->N, P->st);
     P->enq += 1;
 }
 
@@ -167,6 +179,7 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
     ea.W = P->eW;
     ea.mode = P->mode;
     ea.nbx = P->nbx;
+    ea.ncb = P->ncb;
     ea.e_lo = e_lo;
     ea.e_hi = e_hi < 0 ? P->N : e_hi;
     ea.partials = P->partials;
@@ -191,21 +204,21 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
     fz.cond = P->cur_cond;
     fz.B = P->B;
     if (P->egeneral)
-        k_energy<T, SRC_PADDED><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea, fz);
+        klaunch(P, k_energy<T, SRC_PADDED>, dim3(P->nbx, P->B), 256, 0, ea, fz);
     else if (P->eb_px == 1)
-        k_energy_bulk<T, 1><<<dim3(P->nbx, P->B), 288, eb_smem_bytes<T, 1>(P->eb_ns), P->stream>>>(ea, fz, P->eb_H,
+        klaunch(P, k_energy_bulk<T, 1>, dim3(P->nbx, P->B), 288, eb_smem_bytes<T, 1>(P->eb_ns), ea, fz, P->eb_H,
                                                                                                    P->eb_ns);
     else if (P->eb_px == 2)
-        k_energy_bulk<T, 2><<<dim3(P->nbx, P->B), 288, eb_smem_bytes<T, 2>(P->eb_ns), P->stream>>>(ea, fz, P->eb_H,
+        klaunch(P, k_energy_bulk<T, 2>, dim3(P->nbx, P->B), 288, eb_smem_bytes<T, 2>(P->eb_ns), ea, fz, P->eb_H,
                                                                                                    P->eb_ns);
     else if (std::is_same<T, float>::value && P->eb_px == 4)
-        k_energy_bulk<float, 4><<<dim3(P->nbx, P->B), 288, eb_smem_bytes<float, 4>(P->eb_ns), P->stream>>>(
-            ea, fz, P->eb_H, P->eb_ns);
+        klaunch(P, k_energy_bulk<float, 4>, dim3(P->nbx, P->B), 288, eb_smem_bytes<float, 4>(P->eb_ns), ea, fz,
+                P->eb_H, P->eb_ns);
     else
-        k_energy<T, SRC_INPLACE><<<dim3(P->nbx, P->B), 256, 0, P->stream>>>(ea, fz);
+        klaunch(P, k_energy<T, SRC_INPLACE>, dim3(P->nbx, P->B), 256, 0, ea, fz);
     stamp(P, 90);
     if (!P->fused_finalize) {
-        k_finalize<<<P->B, 256, 0, P->stream>>>(P->partials, P->nbx, P->P, P->st, ta, initial);
+        klaunch(P, k_finalize, P->B, 256, 0, P->partials, P->nbx, P->P, P->st, ta, initial);
         P->enq += 1;
         stamp(P, 91);
     }
@@ -273,7 +286,7 @@ void launch_fused(cmg_plan* P, const FusedArgs<T>& a) {
     FusedArgs<T> b = a;
     const int tiles_r = (L.mj + TP - 1) / TP;
     b.tiles_c = (L.nj + TP - 1) / TP;
-    kern<<<dim3(tiles_r * b.tiles_c, 1, P->B), NT, smem, P->stream>>>(b);
+    klaunch(P, kern, dim3(tiles_r * b.tiles_c, 1, P->B), NT, smem, b);
 }
 
 template <typename T>
@@ -297,7 +310,7 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
                 const size_t smem = sizeof(float) * (2 + 8 * G::PLANE);
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
-                kern<<<grd, nt, smem, P->stream>>>(a);
+                klaunch(P, kern, grd, nt, smem, a);
             };
             using I56 = std::integral_constant<int, 56>;
             using I120 = std::integral_constant<int, 120>;
@@ -327,7 +340,7 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
         attr_set = true;
     }
     const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
-    kern<<<grd, 256, smem, P->stream>>>(a);
+    klaunch(P, kern, grd, 256, smem, a);
 }
 
 // shared-memory tile configs of the coarse fused levels (patches per tile
@@ -370,7 +383,7 @@ void launch_coarse(cmg_plan* P, const FusedArgs<T>& a) {
     const bool tma = P->tma_ok[LAYER] && bi >= 0;
     CUtensorMap dummy;
     memset(&dummy, 0, sizeof(dummy));
-    kern<<<grd, C::NT, smem, P->stream>>>(a, tma ? P->tmap[LAYER][bi] : dummy, tma ? P->tmap[LAYER][3] : dummy,
+    klaunch(P, kern, grd, C::NT, smem, a, tma ? P->tmap[LAYER][bi] : dummy, tma ? P->tmap[LAYER][3] : dummy,
                                           tma ? 1 : 0);
 }
 
@@ -382,8 +395,60 @@ inline int coarse_region_impl(int layer) {
     return layer == 2 ? G2::BW * 4096 + G2::RD : G3::BW * 4096 + G3::RD;
 }
 
+// levels 2-3: two launches (patch-row parity 0, then 1), each running its two
+// colours in a shared-memory window (cmg_rowpair.cuh); X -> Y
+template <typename T, int LAYER, int MODE, int PREC, int TS>
+void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
+    using G = RowPairGeom<LAYER, TS>;
+    const Level& L = P->lv[LAYER];
+    RowPairArgs<T> r;
+    r.X = X;
+    r.Y = Y;
+    r.nj = L.nj;
+    r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
+    const size_t smem = sizeof(T) * (G::ROWS + G::S) * G::WIN;  // u window + f of the patch row
+    auto kern = k_rowpair<T, LAYER, MODE, PREC, TS>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    for (int p = 0; p < 2; ++p) {
+        const int rows = (L.mj - p + 1) / 2;
+        if (rows <= 0) continue;
+        r.c0 = make_sweep_args<T>(P, LAYER, 2 * p);
+        r.c1 = make_sweep_args<T>(P, LAYER, 2 * p + 1);
+        klaunch(P, kern, dim3(r.ntiles, rows, P->B), G::NT, smem, r);
+        if (p == 0) {
+            stamp(P, 10 * LAYER + 8);
+        } else {
+            P->enq += 1;  // the caller counts one launch per level
+        }
+    }
+}
+
+template <typename T, int MODE, int PREC>
+void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
+    // team sizes: level 2 {4, 8} lanes per patch, level 3 {8, 16}
+    if (layer == 2) {
+        if (P->ts2 >= 8)
+            launch_rowpair<T, 2, MODE, PREC, 8>(P, a.uin, a.uout);
+        else
+            launch_rowpair<T, 2, MODE, PREC, 4>(P, a.uin, a.uout);
+    } else {
+        if (P->ts3 >= 16)
+            launch_rowpair<T, 3, MODE, PREC, 16>(P, a.uin, a.uout);
+        else
+            launch_rowpair<T, 3, MODE, PREC, 8>(P, a.uin, a.uout);
+    }
+}
+
 template <typename T, int MODE, int PREC>
 void dispatch_fused(cmg_plan* P, int layer, const FusedArgs<T>& a) {
+    if (layer >= 2 && ((P->rowpair >> (layer - 2)) & 1)) {
+        dispatch_rowpair<T, MODE, PREC>(P, layer, a);
+        return;
+    }
     if (layer >= 2 && P->coarse_tile) {
         if (layer == 2)
             launch_coarse<T, 2, MODE, PREC>(P, a);

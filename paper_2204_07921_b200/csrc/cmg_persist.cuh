@@ -339,6 +339,7 @@ __device__ __forceinline__ void phase_finalize(const PersistArgs& a, int initial
 
 template <typename T, int MODE, int PREC, int TS2, int TS3>
 __global__ void __launch_bounds__(256) k_persist(PersistArgs a) {
+    pdl_sync();
     extern __shared__ __align__(16) unsigned char smem[];
     double* sF = reinterpret_cast<double*>(smem);
     int* sdone = reinterpret_cast<int*>(sF + a.B);
@@ -410,6 +411,7 @@ namespace cmg {
 // image is small enough that a colour sweep is latency-bound.
 template <typename T, int MODE, int PREC, int TS2, int TS3>
 __global__ void __launch_bounds__(256) k_coarse_coop(PersistArgs a) {
+    pdl_sync();
     extern __shared__ __align__(16) unsigned char smem[];
     int* sdone = reinterpret_cast<int*>(smem);
     T* sh_rows = reinterpret_cast<T*>(smem + 16 * ((a.B * sizeof(int) + 15) / 16));

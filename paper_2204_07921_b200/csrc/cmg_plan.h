@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cuda.h>
+#include <cstring>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/cmg.h"
@@ -34,6 +36,7 @@ struct cmg_plan {
     cmg::Level lv[7];
     double* partials = nullptr;
     int nbx = 1;
+    int ncb = 1;  // k_energy column chunks (nbx = row bands * ncb)
     int eb_px = 0, eb_ns = 4, eb_H = 32;  // k_energy_bulk<T, eb_px> (0: off)
     cmg::ImgState* st = nullptr;
     int* ndone = nullptr;
@@ -83,12 +86,34 @@ struct cmg_plan {
     int pgrid = 0;          // CTAs of the persistent kernel
     int pcap = 0;           // partials capacity (images*pieces)
     int occ_cap = 4;        // max CTAs per SM for the persistent kernel
+    int rowpair = 3;        // bit j-2: level j (2, 3) runs as two row-parity launches (k_rowpair)
+    bool pdl = true;        // programmatic dependent launch between the cycle's kernels (CMG_PDL=0: off)
 };
 
 namespace cmg {
+// Launch on the plan's stream; with P->pdl the launch carries programmatic
+// stream serialization, so the kernel may be scheduled while its predecessor
+// drains (every kernel begins with pdl_sync(), which waits for it).
+template <typename... KP, typename... Args>
+inline void klaunch(const cmg_plan* P, void (*kern)(KP...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = P->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = P->pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // diagnostics: a 1-thread kernel that appends %globaltimer to a device buffer
 // (CMG_STAMPS=1); placed after every node of the cycle to attribute time
 static __global__ void k_stamp(unsigned long long* buf, int cap, int tag) {
+    pdl_sync();
     const int i = atomicAdd(reinterpret_cast<int*>(buf), 1);
     if (i + 1 < cap) {
         unsigned long long t;

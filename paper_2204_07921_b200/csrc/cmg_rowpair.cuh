@@ -1,0 +1,184 @@
+// cmg_rowpair.cuh -- levels 2-3 as two launches per level visit: one per
+// patch-row parity p, each running the colours (p,0) then (p,1)
+// (driver.sweep_layer, driver.py:225-251, COLOR_ORDER driver.py:35).
+//
+// Why this split is exact.  The stencil of a patch reaches one pixel beyond
+// it, so a colour-(p,1) patch reads the (p,0) patches to its
+// left and right and the patch rows above and below, which have the other
+// parity and are not modified by either colour of this launch.  A CTA owns a
+// patch row and TPC consecutive patch columns; it stages the rows
+// [R0-1, R0+S] of its window (owned patches, one read-only patch on the left,
+// one (p,0) halo patch on the right) in shared memory, runs colour (p,0),
+// refreshes the odd-reflection cells, runs colour (p,1) and writes its owned
+// pixels.  The halo patch is computed redundantly (bit-identical to its
+// owner's result).
+//
+// Buffers: the level reads X and writes Y (the fused-level rotation).  The
+// p=0 launch reads everything from X and writes the parity-0 patch rows of Y;
+// the p=1 launch reads its own rows from X and the parity-0 rows (its ring
+// rows, and mirror rows of the bottom reflection) from Y, where they are
+// final.  No CTA ever reads a pixel another CTA of the same launch writes.
+//
+// Compared with four in-place colour launches this halves the launches and
+// the HBM traffic of a level (each launch reads (S+2)/2S of u and half of f
+// and writes half of u).
+#pragma once
+
+#include "cmg_kernels.cuh"
+
+namespace cmg {
+
+template <typename T>
+struct RowPairArgs {
+    const T* X;      // level input (u before this level)
+    T* Y;            // level output
+    int ntiles;      // column tiles per patch row
+    int nj;          // patch columns
+    SweepArgs<T> c0, c1;  // colours (p,0) and (p,1): p, q, hc, wc, flat, single, backward constants
+};
+
+// shared-memory window accessor in padded image coordinates
+template <typename T>
+struct WinAcc {
+    const T* s;
+    int ld, r0, k0;
+    __device__ __forceinline__ T operator()(int i, int k) const { return s[(i - r0) * ld + (k - k0)]; }
+};
+
+template <int LAYER, int TS>
+struct RowPairGeom {
+    static constexpr int S = (1 << LAYER) - 1;
+    static constexpr int NT = 256;
+    static constexpr int TEAMS = NT / TS;
+    static constexpr int TPC = 2 * TEAMS - 2;          // owned patch columns per CTA (even)
+    static constexpr int WIN = (TPC + 2) * S + 2;      // window columns: [(J0-1)S-1, (J0+TPC+1)S]
+    static constexpr int ROWS = S + 2;                 // window rows: [R0-1, R0+S]
+};
+
+template <typename T, int LAYER, int MODE, int PREC, int TS>
+__global__ void __launch_bounds__(256) k_rowpair(RowPairArgs<T> a) {
+    pdl_sync();
+    using G = RowPairGeom<LAYER, TS>;
+    constexpr int S = G::S;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* win = reinterpret_cast<T*>(smem_raw);
+    const int b = blockIdx.z;
+    const SweepArgs<T>& A0 = a.c0;
+    const int p = A0.p;
+    const int m = A0.m, n = A0.n;
+    const int PR = 2 * blockIdx.y + p;       // patch row
+    const int J0 = blockIdx.x * G::TPC;      // first owned patch column
+    const int R0 = PR * S;
+    const int wr0 = R0 - 1, wk0 = (J0 - 1) * S - 1;  // window origin (padded coordinates)
+    const long long ioff = (long long)b * A0.istride;
+    const T* Xb = a.X + ioff;
+    T* Yb = a.Y + ioff;
+    const T* f = A0.f + ioff;
+    // owned pixels: rows [R0, min(R0+S, m)), columns [J0 S, min((J0+TPC) S, n))
+    const int orow1 = min(R0 + S, m), ok0 = J0 * S, ok1 = min((J0 + G::TPC) * S, n);
+    if (A0.st[b].done) {  // stopped image: carry the owned pixels along the rotation
+        const int w = ok1 - ok0;
+        for (int e = threadIdx.x; e < (orow1 - R0) * w; e += blockDim.x) {
+            const long long g = (long long)(R0 + e / w) * n + ok0 + e % w;
+            Yb[g] = Xb[g];
+        }
+        return;
+    }
+    // pixels of parity-0 patch rows are final in Y during the p=1 launch
+    auto src_row = [&](int i) -> const T* { return (p == 1 && ((i / S) & 1) == 0) ? Yb : Xb; };
+    T* fwin = win + G::ROWS * G::WIN;  // f of window rows 1..S (the patch row), same columns
+    // 1. stage the in-image cells of the window (u rows R0-1 .. R0+S, f rows R0 .. R0+S-1)
+    const int wlo = max(wk0, 0), whi = min(wk0 + G::WIN, n);  // in-image window columns
+    const bool border = (wr0 < 0) || (wr0 + G::ROWS > m) || (wk0 < 0) || (wk0 + G::WIN > n);
+#pragma unroll
+    for (int ri = 0; ri < G::ROWS; ++ri) {
+        const int i = wr0 + ri;
+        if (i < 0 || i >= m) continue;
+        const T* srow = src_row(i) + (long long)i * n;
+        const T* frow = f + (long long)i * n;
+        for (int k = wlo + threadIdx.x; k < whi; k += G::NT) {
+            win[ri * G::WIN + (k - wk0)] = srow[k];
+            if (ri >= 1 && ri <= S) fwin[(ri - 1) * G::WIN + (k - wk0)] = __ldg(frow + k);
+        }
+    }
+    if (border) {  // padded f cells of the patch row (f is constant: reflect from global)
+        const Reflect<T> FR{f, m, n};
+        const int kmax = A0.W - 2;  // np (padded columns run -1 .. np)
+        for (int e = threadIdx.x; e < S * G::WIN; e += G::NT) {
+            const int ri = e / G::WIN, ck = e % G::WIN;
+            const int i = R0 + ri, k = wk0 + ck;
+            if ((i >= m || k == -1 || k >= n) && k >= -1 && k <= kmax) fwin[ri * G::WIN + ck] = FR(i, k);
+        }
+    }
+    // odd reflection (rows first, then columns: tangent.py:262-269) of the window's
+    // out-of-image u cells within one pixel of the padded image; in-image sources come
+    // from the window when inside it, else from the level's stable rows in global memory
+    auto refill = [&]() {
+        auto g = [&](int i, int k) -> T {
+            const int ri = i - wr0, ck = k - wk0;
+            if (ri >= 0 && ri < G::ROWS && ck >= 0 && ck < G::WIN) return win[ri * G::WIN + ck];
+            return src_row(i)[(long long)i * n + k];
+        };
+        auto rowv = [&](int i, int k) -> T {
+            if (i >= 0 && i < m) return g(i, k);
+            const int e = (i < 0) ? 0 : m - 1;
+            const int mi = (i < 0) ? -i : 2 * (m - 1) - i;
+            return X<T>::sub(X<T>::mul(T(2), g(e, k)), g(mi, k));
+        };
+        for (int ri = 0; ri < G::ROWS; ++ri) {  // rows beyond the image, in-image columns
+            const int i = wr0 + ri;
+            if (i >= 0 && i < m) continue;
+            for (int k = wlo + threadIdx.x; k < whi; k += G::NT) win[ri * G::WIN + (k - wk0)] = rowv(i, k);
+        }
+        __syncthreads();
+        // columns beyond the image (column -1 and n .. np): reflect the row-padded values
+        const int kmax = A0.W - 2;
+        const int klo = max(wk0, n), khi = min(wk0 + G::WIN - 1, kmax);
+        for (int ri = threadIdx.x / 32; ri < G::ROWS; ri += G::NT / 32) {
+            const int i = wr0 + ri;
+            for (int k = klo + (threadIdx.x & 31); k <= khi; k += 32)
+                win[ri * G::WIN + (k - wk0)] =
+                    X<T>::sub(X<T>::mul(T(2), rowv(i, n - 1)), rowv(i, 2 * (n - 1) - k));
+            if (wk0 <= -1 && (threadIdx.x & 31) == 0)
+                win[ri * G::WIN + (-1 - wk0)] = X<T>::sub(X<T>::mul(T(2), rowv(i, 0)), rowv(i, 1));
+        }
+        __syncthreads();
+    };
+    __syncthreads();
+    if (border) refill();
+    const WinAcc<T> U{win, G::WIN, wr0, wk0};
+    const WinAcc<T> F{fwin, G::WIN, R0, wk0};
+    const int lane = threadIdx.x % TS, team = threadIdx.x / TS;
+    bool bad = false;
+    // 2. the two colours of this patch row: (p,0) on J0, J0+2, ..., J0+TPC (the last one
+    // is the halo the (p,1) patch J0+TPC-1 needs), then (p,1) on J0+1, ..., J0+TPC-1
+    static_for<0, 2>([&](auto qc) {
+        constexpr int q = decltype(qc)::value;
+        const SweepArgs<T>& A = q ? a.c1 : a.c0;
+        const int J = J0 + q + 2 * team;
+        const bool active = (J < a.nj) && (q == 0 ? J <= J0 + G::TPC : J < J0 + G::TPC) && A.wc > 0;
+        if (__any_sync(0xffffffffu, active)) {
+            const int Jc = active ? J : J0;  // inactive teams shadow a valid patch (converged shuffles)
+            const int C0 = Jc * S;
+            const T c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, A);
+            if (active) {
+                if (lane == 0 && !isfinite(c)) bad = true;
+                for (int e = lane; e < S * S; e += TS) {
+                    const int i = R0 + e / S, k = C0 + e % S;
+                    if (i < m && k < n) {
+                        T* px = win + (i - wr0) * G::WIN + (k - wk0);
+                        *px = X<T>::add(*px, c);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (q == 0 && border) refill();
+    });
+    if (bad) A0.st[b].bad = 1;
+    // 3. owned pixels -> Y
+    for (int i = R0; i < orow1; ++i)
+        for (int k = ok0 + threadIdx.x; k < ok1; k += G::NT) Yb[(long long)i * n + k] = win[(i - wr0) * G::WIN + (k - wk0)];
+}
+
+}  // namespace cmg
