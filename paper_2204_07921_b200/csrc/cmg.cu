@@ -602,6 +602,10 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     CKP(cudaMemset(P->tickets, 0, sizeof(int) * (batch + 1)));
     if (const char* ff = getenv("CMG_FUSED_FINALIZE")) P->fused_finalize = atoi(ff) != 0;
     if (const char* pd = getenv("CMG_PDL")) P->pdl = atoi(pd) != 0;
+    // 32 x 64 level-1 tiles once they fill the GPU (1024^2 fp64 exact: 48.7 -> 47.3 us,
+    // 4096^2: 643 -> 579 us; 512^2 has too few: 20.3 -> 27.2 us)
+    P->l1_wide = (long long)batch * m * n >= (1LL << 20);
+    if (const char* lw = getenv("CMG_L1_WIDE")) P->l1_wide = atoi(lw) != 0;
     CKP(cudaMalloc(&P->P, sizeof(SolveParams)));
 #undef CKP
     *out = P;

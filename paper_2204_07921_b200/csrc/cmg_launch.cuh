@@ -330,17 +330,25 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
             return;
         }
     }
-    constexpr int TH = L1Tile<T>::TH, TW = L1Tile<T>::TW;
-    using G = L1Geom<T, TH, TW>;
-    const size_t smem = 2 * sizeof(T) * 4 * G::PLANE;
-    auto kern = k_l1_tile<T, MODE, PREC, TH, TW>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
-    const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
-    klaunch(P, kern, grd, 256, smem, a);
+    auto go = [&](auto th, auto tw) {
+        constexpr int TH = decltype(th)::value, TW = decltype(tw)::value;
+        using G = L1Geom<T, TH, TW>;
+        const size_t smem = 2 * sizeof(T) * 4 * G::PLANE;
+        auto kern = k_l1_tile<T, MODE, PREC, TH, TW>;
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_set = true;
+        }
+        const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
+        klaunch(P, kern, grd, 256, smem, a);
+    };
+    using IH = std::integral_constant<int, L1Tile<T>::TH>;
+    using IW = std::integral_constant<int, L1Tile<T>::TW>;
+    if (P->l1_wide)  // 32 x 64 tiles: fewer CTAs (one wave at 1024^2 fp64), less halo per pixel
+        go(std::integral_constant<int, 32>{}, std::integral_constant<int, 64>{});
+    else
+        go(IH{}, IW{});
 }
 
 // shared-memory tile configs of the coarse fused levels (patches per tile

@@ -55,55 +55,84 @@ struct RowPairGeom {
     static constexpr int ROWS = S + 2;                 // window rows: [R0-1, R0+S]
 };
 
-template <typename T, int LAYER, int MODE, int PREC, int TS>
-__global__ void __launch_bounds__(256) k_rowpair(RowPairArgs<T> a) {
-    pdl_sync();
+// one work item: patch row PR of image b, owned patch columns [J0, J0+TPC)
+template <typename T>
+struct RPItem {
+    int b, R0, J0, wr0, wk0, orow1, ok0, ok1;
+    bool border;
+    const T *Xb, *f;
+    T* Yb;
+};
+
+template <typename T, int LAYER, int TS>
+__device__ __forceinline__ RPItem<T> rp_item(const RowPairArgs<T>& a, int b, int pr, int tile) {
     using G = RowPairGeom<LAYER, TS>;
     constexpr int S = G::S;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* win = reinterpret_cast<T*>(smem_raw);
-    const int b = blockIdx.z;
     const SweepArgs<T>& A0 = a.c0;
-    const int p = A0.p;
     const int m = A0.m, n = A0.n;
-    const int PR = 2 * blockIdx.y + p;       // patch row
-    const int J0 = blockIdx.x * G::TPC;      // first owned patch column
-    const int R0 = PR * S;
-    const int wr0 = R0 - 1, wk0 = (J0 - 1) * S - 1;  // window origin (padded coordinates)
-    const long long ioff = (long long)b * A0.istride;
-    const T* Xb = a.X + ioff;
-    T* Yb = a.Y + ioff;
-    const T* f = A0.f + ioff;
+    RPItem<T> it;
+    it.b = b;
+    it.R0 = (2 * pr + A0.p) * S;
+    it.J0 = tile * G::TPC;
+    it.wr0 = it.R0 - 1;
+    it.wk0 = (it.J0 - 1) * S - 1;  // window origin (padded coordinates)
     // owned pixels: rows [R0, min(R0+S, m)), columns [J0 S, min((J0+TPC) S, n))
-    const int orow1 = min(R0 + S, m), ok0 = J0 * S, ok1 = min((J0 + G::TPC) * S, n);
-    if (A0.st[b].done) {  // stopped image: carry the owned pixels along the rotation
-        const int w = ok1 - ok0;
-        for (int e = threadIdx.x; e < (orow1 - R0) * w; e += blockDim.x) {
-            const long long g = (long long)(R0 + e / w) * n + ok0 + e % w;
-            Yb[g] = Xb[g];
-        }
-        return;
-    }
-    // pixels of parity-0 patch rows are final in Y during the p=1 launch
-    auto src_row = [&](int i) -> const T* { return (p == 1 && ((i / S) & 1) == 0) ? Yb : Xb; };
-    T* fwin = win + G::ROWS * G::WIN;  // f of window rows 1..S (the patch row), same columns
-    // 1. stage the in-image cells of the window (u rows R0-1 .. R0+S, f rows R0 .. R0+S-1)
-    const int wlo = max(wk0, 0), whi = min(wk0 + G::WIN, n);  // in-image window columns
-    const bool border = (wr0 < 0) || (wr0 + G::ROWS > m) || (wk0 < 0) || (wk0 + G::WIN > n);
+    it.orow1 = min(it.R0 + S, m);
+    it.ok0 = it.J0 * S;
+    it.ok1 = min((it.J0 + G::TPC) * S, n);
+    it.border = (it.wr0 < 0) || (it.wr0 + G::ROWS > m) || (it.wk0 < 0) || (it.wk0 + G::WIN > n);
+    const long long ioff = (long long)b * A0.istride;
+    it.Xb = a.X + ioff;
+    it.Yb = a.Y + ioff;
+    it.f = A0.f + ioff;
+    return it;
+}
+
+// pixels of parity-0 patch rows are final in Y during the p=1 launch
+template <typename T, int S>
+__device__ __forceinline__ const T* rp_src_row(const RPItem<T>& it, int p, int i) {
+    return (p == 1 && ((i / S) & 1) == 0) ? it.Yb : it.Xb;
+}
+
+// stage the in-image cells of an item's window: u rows R0-1 .. R0+S into win,
+// f rows R0 .. R0+S-1 into fwin = win + ROWS*WIN.
+template <typename T, int LAYER, int TS>
+__device__ __forceinline__ void rp_stage(const RowPairArgs<T>& a, const RPItem<T>& it, T* win) {
+    using G = RowPairGeom<LAYER, TS>;
+    constexpr int S = G::S;
+    const int m = a.c0.m, n = a.c0.n, p = a.c0.p;
+    T* fwin = win + G::ROWS * G::WIN;
+    const int wlo = max(it.wk0, 0), whi = min(it.wk0 + G::WIN, n);  // in-image window columns
 #pragma unroll
     for (int ri = 0; ri < G::ROWS; ++ri) {
-        const int i = wr0 + ri;
+        const int i = it.wr0 + ri;
         if (i < 0 || i >= m) continue;
-        const T* srow = src_row(i) + (long long)i * n;
-        const T* frow = f + (long long)i * n;
+        const T* srow = rp_src_row<T, S>(it, p, i) + (long long)i * n;
+        const T* frow = it.f + (long long)i * n;
         for (int k = wlo + threadIdx.x; k < whi; k += G::NT) {
-            win[ri * G::WIN + (k - wk0)] = srow[k];
-            if (ri >= 1 && ri <= S) fwin[(ri - 1) * G::WIN + (k - wk0)] = __ldg(frow + k);
+            T* du = win + ri * G::WIN + (k - it.wk0);
+            T* df = fwin + (ri - 1) * G::WIN + (k - it.wk0);
+            *du = srow[k];
+            if (ri >= 1 && ri <= S) *df = __ldg(frow + k);
         }
     }
-    if (border) {  // padded f cells of the patch row (f is constant: reflect from global)
-        const Reflect<T> FR{f, m, n};
-        const int kmax = A0.W - 2;  // np (padded columns run -1 .. np)
+}
+
+// everything after staging: border refills, the two colours, write-back.
+// Starts and ends with the window consistent across the CTA (callers sync
+// before; this ends with a barrier-free write-back of owned pixels).
+template <typename T, int LAYER, int MODE, int PREC, int TS>
+__device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem<T>& it, T* win) {
+    using G = RowPairGeom<LAYER, TS>;
+    constexpr int S = G::S;
+    const SweepArgs<T>& A0 = a.c0;
+    const int m = A0.m, n = A0.n, p = A0.p;
+    const int R0 = it.R0, J0 = it.J0, wr0 = it.wr0, wk0 = it.wk0;
+    T* fwin = win + G::ROWS * G::WIN;
+    const int wlo = max(wk0, 0), whi = min(wk0 + G::WIN, n);
+    const int kmax = A0.W - 2;  // np (padded columns run -1 .. np)
+    if (it.border) {  // padded f cells of the patch row (f is constant: reflect from global)
+        const Reflect<T> FR{it.f, m, n};
         for (int e = threadIdx.x; e < S * G::WIN; e += G::NT) {
             const int ri = e / G::WIN, ck = e % G::WIN;
             const int i = R0 + ri, k = wk0 + ck;
@@ -117,7 +146,7 @@ __global__ void __launch_bounds__(256) k_rowpair(RowPairArgs<T> a) {
         auto g = [&](int i, int k) -> T {
             const int ri = i - wr0, ck = k - wk0;
             if (ri >= 0 && ri < G::ROWS && ck >= 0 && ck < G::WIN) return win[ri * G::WIN + ck];
-            return src_row(i)[(long long)i * n + k];
+            return rp_src_row<T, S>(it, p, i)[(long long)i * n + k];
         };
         auto rowv = [&](int i, int k) -> T {
             if (i >= 0 && i < m) return g(i, k);
@@ -132,7 +161,6 @@ __global__ void __launch_bounds__(256) k_rowpair(RowPairArgs<T> a) {
         }
         __syncthreads();
         // columns beyond the image (column -1 and n .. np): reflect the row-padded values
-        const int kmax = A0.W - 2;
         const int klo = max(wk0, n), khi = min(wk0 + G::WIN - 1, kmax);
         for (int ri = threadIdx.x / 32; ri < G::ROWS; ri += G::NT / 32) {
             const int i = wr0 + ri;
@@ -144,13 +172,12 @@ __global__ void __launch_bounds__(256) k_rowpair(RowPairArgs<T> a) {
         }
         __syncthreads();
     };
-    __syncthreads();
-    if (border) refill();
+    if (it.border) refill();
     const WinAcc<T> U{win, G::WIN, wr0, wk0};
     const WinAcc<T> F{fwin, G::WIN, R0, wk0};
     const int lane = threadIdx.x % TS, team = threadIdx.x / TS;
     bool bad = false;
-    // 2. the two colours of this patch row: (p,0) on J0, J0+2, ..., J0+TPC (the last one
+    // the two colours of this patch row: (p,0) on J0, J0+2, ..., J0+TPC (the last one
     // is the halo the (p,1) patch J0+TPC-1 needs), then (p,1) on J0+1, ..., J0+TPC-1
     static_for<0, 2>([&](auto qc) {
         constexpr int q = decltype(qc)::value;
@@ -173,12 +200,40 @@ __global__ void __launch_bounds__(256) k_rowpair(RowPairArgs<T> a) {
             }
         }
         __syncthreads();
-        if (q == 0 && border) refill();
+        if (q == 0 && it.border) refill();
     });
-    if (bad) A0.st[b].bad = 1;
-    // 3. owned pixels -> Y
-    for (int i = R0; i < orow1; ++i)
-        for (int k = ok0 + threadIdx.x; k < ok1; k += G::NT) Yb[(long long)i * n + k] = win[(i - wr0) * G::WIN + (k - wk0)];
+    if (bad) A0.st[it.b].bad = 1;
+    // owned pixels -> Y
+    for (int i = R0; i < it.orow1; ++i)
+        for (int k = it.ok0 + threadIdx.x; k < it.ok1; k += G::NT)
+            it.Yb[(long long)i * n + k] = win[(i - wr0) * G::WIN + (k - wk0)];
+}
+
+// stopped image: carry the owned pixels along the buffer rotation
+template <typename T, int LAYER, int TS>
+__device__ __forceinline__ void rp_copy_owned(const RowPairArgs<T>& a, const RPItem<T>& it) {
+    using G = RowPairGeom<LAYER, TS>;
+    const int n = a.c0.n;
+    for (int i = it.R0; i < it.orow1; ++i)
+        for (int k = it.ok0 + threadIdx.x; k < it.ok1; k += G::NT) {
+            const long long g = (long long)i * n + k;
+            it.Yb[g] = it.Xb[g];
+        }
+}
+
+template <typename T, int LAYER, int MODE, int PREC, int TS>
+__global__ void __launch_bounds__(256) k_rowpair(RowPairArgs<T> a) {
+    pdl_sync();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* win = reinterpret_cast<T*>(smem_raw);
+    const RPItem<T> it = rp_item<T, LAYER, TS>(a, blockIdx.z, blockIdx.y, blockIdx.x);
+    if (a.c0.st[it.b].done) {
+        rp_copy_owned<T, LAYER, TS>(a, it);
+        return;
+    }
+    rp_stage<T, LAYER, TS>(a, it, win);
+    __syncthreads();
+    rp_compute<T, LAYER, MODE, PREC, TS>(a, it, win);
 }
 
 }  // namespace cmg
