@@ -397,8 +397,14 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": int(alg_bytes), "launch_ms": l1_ms, "peak_source": peak_src},
         "clocks": clocks,
     }
+    if args.config == 3 and args.dtype == "float64" and args.precision == "exact":
+        line["roofline"]["note"] = ("1024^2 fp64 exact: u and f (16 MiB) stay in the 126 MB L2 and the level-1 "
+                                    "kernel is FP64-pipe bound (8 correctly rounded sqrt + div per pixel, ncu "
+                                    "profiles/r01/ncu); the HBM roofline binds at 16384^2: roofline_fine_level")
     if rank == 0 and ws == 1 and not args.no_fine and args.config != 5:
         line["roofline_fine_level"] = fine_level_roofline(local, peak)
+    if rank == 0 and ws == 1 and args.config == 3 and not args.no_fine:
+        line["config"]["other_precisions"] = other_precisions(local, args.steps)
     if cpu:
         line["cpu_baseline"] = cpu
     if rank == 0:
@@ -416,6 +422,38 @@ def l1_kernel_name(dtype: str, prec: str, m: int, n: int) -> str:
         return f"k_l1_x2<{tile}> (level-1 sweep, four colours in one launch, packed f32x2)"
     t = "double" if dtype == "float64" else "float"
     return f"k_l1_tile<{t}, {prec}> (level-1 sweep, four colours in one launch)"
+
+
+def other_precisions(local: int, steps: int) -> dict:
+    """Config 3 in the other modes, device-timed like the headline: fp64 with the
+    closed-form curvature (north_star fp64 bar: energy 1e-9 rel, image 1e-8
+    max-abs; tests/test_gpu_parity.py) and fp32 (energy 1e-4 rel, PSNR 0.05 dB)."""
+    from paper_2204_07921_b200 import _native as N
+    from paper_2204_07921_b200 import synth
+
+    out = {}
+    for dt, prec in (("float64", "fast"), ("float32", "fast")):
+        f, _ = synth.config_input(3, 0, fp32=(dt == "float32"))
+        p = N.Plan(1024, 1024, 1, 3, "mean", dt, prec, device=local)
+        fh = np.ascontiguousarray(f[None].astype(dt))
+        assert N.lib().cmg_buffer_upload(p.handle, 3, N.ptr(fh)) == 0
+        en = np.zeros(64)
+        its = np.zeros(1, dtype=np.int32)
+        sts = np.zeros(1, dtype=np.int32)
+
+        def solve():
+            rc = N.lib().cmg_solve_device(p.handle, None, None, None, 0.06, 1e-6, 60, 1, 0, 0, 1.0, N.dptr(en),
+                                          None, None, None, None, N.iptr(its), N.iptr(sts))
+            assert rc in (0, 2), N.last_error()
+            return p.stats()["device_ms"]
+
+        for _ in range(3):
+            solve()
+        ms = float(np.mean([solve() for _ in range(max(steps, 3))]))
+        out[f"{dt}_{prec}"] = {"time_to_tolerance_ms": ms, "cycles": int(its[0]),
+                               "Mpixel_sweeps_per_s": int(its[0]) * 3 * 1024 * 1024 / (ms * 1e-3) / 1e6}
+        p.close()
+    return out
 
 
 def fine_level_roofline(local: int, peak: float) -> dict:

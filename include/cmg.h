@@ -139,6 +139,18 @@ int cmg_level_step(cmg_plan* plan, int layer, int in_index, int out_index, doubl
 int cmg_energy_partials(cmg_plan* plan, int u_index, int prev_index, int use_ref, int row_lo, int row_hi,
                         double* out);
 
+/*
+ * curvemg.image.ssim (image.py:152-192) on the GPU, bit-identical: mean SSIM
+ * of batch image pairs (batch*m*n row-major, dtype 0 f64 / 1 f32, values
+ * taken as float64), 11x11 Gaussian windows.  The caller passes the window
+ * (_gaussian_window(11, 1.5), image.py:157-160) and c1 = (0.01 peak)^2,
+ * c2 = (0.03 peak)^2 computed as the reference does.  out[batch].
+ */
+int cmg_ssim_batch(int batch, int m, int n, int dtype, const void* a_host, const void* b_host, const double* window,
+                   double c1, double c2, double* out);
+/* the same on two of a plan's device buffers (0..2 u rotation, 3 f, 4 reference) */
+int cmg_plan_ssim(cmg_plan* plan, int a_index, int b_index, const double* window, double c1, double c2, double* out);
+
 /* Pinned host memory helpers (for host<->device copies at full PCIe rate). */
 void* cmg_host_alloc(unsigned long long bytes);
 int cmg_host_free(void* p);

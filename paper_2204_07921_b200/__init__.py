@@ -18,7 +18,8 @@ from .driver import (
     rel_err_energy,
     rel_err_u,
 )
-from .image import Image, NoiseSpec, add_gaussian_noise, psnr, ssim
+from .image import Image, NoiseSpec, add_gaussian_noise, psnr
+from .metrics import ssim, ssim_batch
 from .planes import planes as plane_table
 
 __all__ = [
@@ -36,6 +37,7 @@ __all__ = [
     "add_gaussian_noise",
     "psnr",
     "ssim",
+    "ssim_batch",
     "plane_table",
 ]
 

@@ -24,7 +24,7 @@ SYMBOLS = (
     "cmg_version", "cmg_last_error", "cmg_device_count", "cmg_plan_create", "cmg_plan_destroy", "cmg_solve",
     "cmg_solve_device", "cmg_sweep_layer", "cmg_energy", "cmg_plane_table", "cmg_plan_stats", "cmg_time_sweep",
     "cmg_host_alloc", "cmg_host_free", "cmg_plan_buffer", "cmg_buffer_upload", "cmg_buffer_download",
-    "cmg_level_step", "cmg_energy_partials",
+    "cmg_level_step", "cmg_energy_partials", "cmg_ssim_batch", "cmg_plan_ssim",
 )
 
 
@@ -81,6 +81,10 @@ def _declare(L):
     L.cmg_level_step.argtypes = [_vp, _i, _i, _i, _d, _i]
     L.cmg_energy_partials.restype = _i
     L.cmg_energy_partials.argtypes = [_vp, _i, _i, _i, _i, _i, _dp]
+    L.cmg_ssim_batch.restype = _i
+    L.cmg_ssim_batch.argtypes = [_i, _i, _i, _i, _vp, _vp, _dp, _d, _d, _dp]
+    L.cmg_plan_ssim.restype = _i
+    L.cmg_plan_ssim.argtypes = [_vp, _i, _i, _dp, _d, _d, _dp]
 
 
 def lib():

@@ -25,6 +25,7 @@
 
 #include "../../include/cmg.h"
 #include "cmg_plan.h"
+#include "cmg_metrics.cuh"
 
 using namespace cmg;
 
@@ -788,6 +789,111 @@ static void* buffer_ptr(cmg_plan* P, int index) {
         return P->ref;
     }
     return nullptr;
+}
+
+// NumPy pairwise summation tree (numpy/_core/src/umath/loops_utils.h.src):
+// leaves of <= 128 elements in evaluation order, then the same recursion over
+// the leaf sums
+static void pairwise_leaves(long long off, long long n, std::vector<long long>& lo, std::vector<int>& ln) {
+    if (n <= 128) {
+        lo.push_back(off);
+        ln.push_back((int)n);
+        return;
+    }
+    long long n2 = n / 2;
+    n2 -= n2 % 8;
+    pairwise_leaves(off, n2, lo, ln);
+    pairwise_leaves(off + n2, n - n2, lo, ln);
+}
+static double pairwise_combine(long long n, const double* leaf, size_t& next) {
+    if (n <= 128) return leaf[next++];
+    long long n2 = n / 2;
+    n2 -= n2 % 8;
+    const double l = pairwise_combine(n2, leaf, next);
+    const double r = pairwise_combine(n - n2, leaf, next);
+    return l + r;
+}
+
+// SSIM of batch image pairs already on the device (see cmg_metrics.cuh)
+static int ssim_device(int batch, int m, int n, int dtype, const void* a, const void* b, const double* window,
+                       double c1, double c2, double* out, cudaStream_t st) {
+    const long long nout = (long long)(m - 10) * (n - 10);
+    std::vector<long long> lo;
+    std::vector<int> ln;
+    pairwise_leaves(0, nout, lo, ln);
+    const int nl = (int)lo.size();
+    double *map = nullptr, *leaf = nullptr;
+    long long* dlo = nullptr;
+    int* dln = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(map);
+        cudaFree(leaf);
+        cudaFree(dlo);
+        cudaFree(dln);
+    };
+    cudaError_t e = cudaMalloc(&map, sizeof(double) * nout * batch);
+    if (e == cudaSuccess) e = cudaMalloc(&leaf, sizeof(double) * nl * batch);
+    if (e == cudaSuccess) e = cudaMalloc(&dlo, sizeof(long long) * nl);
+    if (e == cudaSuccess) e = cudaMalloc(&dln, sizeof(int) * nl);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dlo, lo.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dln, ln.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+        cleanup();
+        return fail(CMG_ECUDA, cudaGetErrorString(e));
+    }
+    cmg::SsimArgs sa;
+    for (int i = 0; i < 11; ++i) sa.w[i] = window[i];
+    sa.c1 = c1;
+    sa.c2 = c2;
+    sa.m = m;
+    sa.n = n;
+    const dim3 g1((unsigned)((nout + 255) / 256), batch);
+    if (dtype == CMG_F64)
+        cmg::k_ssim_map<double><<<g1, 256, 0, st>>>((const double*)a, (const double*)b, map, sa);
+    else
+        cmg::k_ssim_map<float><<<g1, 256, 0, st>>>((const float*)a, (const float*)b, map, sa);
+    cmg::k_pairwise_leaves<<<dim3((nl + 255) / 256, batch), 256, 0, st>>>(map, nout, dlo, dln, nl, leaf);
+    std::vector<double> hl((size_t)nl * batch);
+    e = cudaMemcpyAsync(hl.data(), leaf, sizeof(double) * nl * batch, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cleanup();
+    if (e != cudaSuccess) return fail(CMG_ECUDA, cudaGetErrorString(e));
+    for (int bb = 0; bb < batch; ++bb) {
+        size_t next = 0;
+        out[bb] = pairwise_combine(nout, hl.data() + (size_t)bb * nl, next) / (double)nout;  // np.mean
+    }
+    return CMG_OK;
+}
+
+int cmg_ssim_batch(int batch, int m, int n, int dtype, const void* a_host, const void* b_host, const double* window,
+                   double c1, double c2, double* out) {
+    if (!a_host || !b_host || !window || !out) return fail(CMG_EINVAL, "NULL argument");
+    if (batch < 1) return fail(CMG_EINVAL, "batch must be positive");
+    if (dtype != CMG_F64 && dtype != CMG_F32) return fail(CMG_EINVAL, "dtype must be f64 or f32");
+    if (m < 11 || n < 11) return fail(CMG_EINVAL, "image smaller than the 11x11 SSIM window");
+    const size_t bytes = (size_t)(dtype == CMG_F64 ? 8 : 4) * m * n * batch;
+    void *da = nullptr, *db = nullptr;
+    cudaError_t e = cudaMalloc(&da, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&db, bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(da, a_host, bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(db, b_host, bytes, cudaMemcpyHostToDevice);
+    int rc = (e == cudaSuccess) ? ssim_device(batch, m, n, dtype, da, db, window, c1, c2, out, 0)
+                                : fail(CMG_ECUDA, cudaGetErrorString(e));
+    cudaFree(da);
+    cudaFree(db);
+    return rc;
+}
+
+int cmg_plan_ssim(cmg_plan* P, int a_index, int b_index, const double* window, double c1, double c2, double* out) {
+    if (!P || !window || !out) return fail(CMG_EINVAL, "NULL argument");
+    int rc = set_device(P);
+    if (rc) return rc;
+    if (P->m < 11 || P->n < 11) return fail(CMG_EINVAL, "image smaller than the 11x11 SSIM window");
+    const void* a = buffer_ptr(P, a_index);
+    const void* b = buffer_ptr(P, b_index);
+    if (!a || !b) return fail(CMG_EINVAL, "buffer index must be 0..4");
+    return ssim_device(P->B, P->m, P->n, P->dtype, a, b, window, c1, c2, out, P->stream);
 }
 
 int cmg_plan_buffer(cmg_plan* P, int index, void** dev_ptr) {

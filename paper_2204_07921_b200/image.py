@@ -7,8 +7,8 @@ Mirrors the reference ``curvemg.image`` names the solver boundary uses
 * ``NoiseSpec``          image.py:78-87
 * ``add_gaussian_noise`` image.py:124-134 (default_rng(seed).normal, unclipped)
 * ``psnr``               image.py:140-149
-* ``ssim``               image.py:152-192
 
+SSIM runs on the GPU (``metrics.ssim``, bit-identical to image.py:152-192).
 Everything here is host-side NumPy; none of it is on the timed GPU path.
 """
 
@@ -19,7 +19,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["Image", "NoiseSpec", "add_gaussian_noise", "psnr", "ssim"]
+__all__ = ["Image", "NoiseSpec", "add_gaussian_noise", "psnr"]
 
 
 @dataclass(frozen=True)
@@ -92,34 +92,3 @@ def psnr(a: Image, b: Image) -> float:
     if mse == 0.0:
         return math.inf
     return 10.0 * math.log10(a.peak * a.peak / mse)
-
-
-def _gauss_window(size: int = 11, sigma: float = 1.5) -> np.ndarray:
-    x = np.arange(size, dtype=np.float64) - (size - 1) / 2.0
-    g = np.exp(-(x * x) / (2.0 * sigma * sigma))
-    return g / g.sum()
-
-
-def _valid_filter(arr: np.ndarray, w: np.ndarray) -> np.ndarray:
-    k = w.size
-    rows = sum(w[i] * arr[i: arr.shape[0] - k + 1 + i, :] for i in range(k))
-    return sum(w[i] * rows[:, i: arr.shape[1] - k + 1 + i] for i in range(k))
-
-
-def ssim(a: Image, b: Image) -> float:
-    """Mean SSIM over 11x11 Gaussian windows, sigma 1.5, K1=.01, K2=.03 (image.py:152-192)."""
-    if a.shape != b.shape:
-        raise ValueError(f"shape mismatch: {a.shape} vs {b.shape}")
-    if min(a.shape) < 11:
-        raise ValueError("image smaller than the 11x11 SSIM window")
-    w = _gauss_window()
-    x, y = a.data, b.data
-    mx, my = _valid_filter(x, w), _valid_filter(y, w)
-    vx = _valid_filter(x * x, w) - mx * mx
-    vy = _valid_filter(y * y, w) - my * my
-    cxy = _valid_filter(x * y, w) - mx * my
-    c1 = (0.01 * a.peak) ** 2
-    c2 = (0.03 * a.peak) ** 2
-    num = (2.0 * mx * my + c1) * (2.0 * cxy + c2)
-    den = (mx * mx + my * my + c1) * (vx + vy + c2)
-    return float(np.mean(num / den))

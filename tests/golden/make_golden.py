@@ -162,6 +162,38 @@ def configs_fixture():
     (HERE / "configs.json").write_text(json.dumps(out, indent=1))
 
 
+def metrics_io_fixture():
+    """SSIM / PSNR of seeded image pairs (curvemg.image, image.py:140-192) and the
+    reference's own PGM (8/16-bit) and CSV+JSON files of one small image
+    (image.py:289-335), read back by the reference."""
+    from curvemg import image as I
+
+    rng = np.random.default_rng(77)
+    cases, arrays = [], {}
+    for k, (m, n, peak, dt) in enumerate([(11, 11, 1.0, "f8"), (11, 40, 1.0, "f8"), (37, 53, 255.0, "f8"),
+                                          (128, 128, 1.0, "f8"), (200, 256, 1.0, "f4"), (64, 96, 255.0, "f4")]):
+        x = rng.uniform(0, peak, (m, n))
+        y = np.clip(x + rng.normal(0, 0.1 * peak, (m, n)), 0, peak)
+        x, y = x.astype(dt).astype(np.float64), y.astype(dt).astype(np.float64)
+        a, b = I.Image(x, peak), I.Image(y, peak)
+        arrays[f"x{k}"], arrays[f"y{k}"] = x, y
+        cases.append(dict(shape=[m, n], peak=peak, dtype=dt, ssim=I.ssim(a, b), psnr=I.psnr(a, b),
+                          ssim_self=I.ssim(a, a)))
+    np.savez_compressed(HERE / "metrics.npz", **arrays)
+    (HERE / "metrics.json").write_text(json.dumps(cases, indent=1))
+    io_dir = HERE / "io"
+    io_dir.mkdir(exist_ok=True)
+    img = I.Image(np.clip(rng.normal(120, 60, (17, 23)), -10, 300), 255.0)
+    np.save(io_dir / "image.npy", img.data)
+    I.write_pgm(img, io_dir / "img8.pgm", bits=8)
+    I.write_pgm(img, io_dir / "img16.pgm", bits=16)
+    I.write_csv(img, io_dir / "img.csv")
+    back = {name: I.read_pgm(io_dir / name) for name in ("img8.pgm", "img16.pgm")}
+    np.savez_compressed(io_dir / "read_back.npz", img8=back["img8.pgm"].data, img16=back["img16.pgm"].data,
+                        csv=I.read_csv(io_dir / "img.csv").data)
+    (io_dir / "read_back.json").write_text(json.dumps({k: v.peak for k, v in back.items()}))
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", action="store_true")
@@ -172,3 +204,4 @@ if __name__ == "__main__":
         planes_fixture()
         sweeps_fixture()
         denoise_fixture()
+        metrics_io_fixture()
