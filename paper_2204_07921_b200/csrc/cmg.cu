@@ -454,11 +454,15 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     // levels 2-3 as two row-parity launches each (k_rowpair): half the launches and
     // half the traffic of four colour launches; they join the fused X -> Y rotation
     // measured (B200, round 1): a win for latency-bound jobs (1024^2 fp64 fast: 4.13 -> 3.80 ms
-    // per solve; exact: level 3 only), a loss for large throughput-bound jobs (16384^2 level 2:
+    // per solve), a loss for large throughput-bound jobs (16384^2 level 2:
     // 3.6 vs 1.3 ms with the coarse tile), where the per-colour / tile kernels stay
     const bool small_job = (long long)batch * m * n < (4LL << 20);
-    P->rowpair = small_job ? (precision == CMG_PREC_FAST && mode == CMG_MODE_MEAN ? 3 : 2) : 0;
+    // (bench, config 3: fp64 exact 5.24 ms with 8-lane level-2 teams vs 5.04 ms with 4;
+    // fp64 fast 3.92 vs 3.75; configs 1 / 2: 2.69 -> 2.61 ms, 18.7 -> 18.1 ms with row pairs)
+    P->rowpair = small_job ? 3 : 0;
+    P->rp_ts2 = 4;
     if (const char* rp = getenv("CMG_ROWPAIR")) P->rowpair = atoi(rp) & 3;
+    if (const char* rt = getenv("CMG_RP_TS2")) P->rp_ts2 = atoi(rt);
     if (layers >= 2 && (P->rowpair & 1)) P->fuse_mask |= 2;
     if (layers >= 3 && (P->rowpair & 2)) P->fuse_mask |= 4;
     if (const char* fm = getenv("CMG_FUSE_MASK")) P->fuse_mask = atoi(fm) | 1;

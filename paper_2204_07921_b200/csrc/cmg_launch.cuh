@@ -437,9 +437,9 @@ void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
 
 template <typename T, int MODE, int PREC>
 void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
-    // team sizes: level 2 {4, 8} lanes per patch, level 3 {8, 16}
+    // team sizes: level 2 {4, 8} lanes per patch (P->rp_ts2), level 3 {8, 16}
     if (layer == 2) {
-        if (P->ts2 >= 8)
+        if (P->rp_ts2 >= 8)
             launch_rowpair<T, 2, MODE, PREC, 8>(P, a.uin, a.uout);
         else
             launch_rowpair<T, 2, MODE, PREC, 4>(P, a.uin, a.uout);

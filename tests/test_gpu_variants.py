@@ -34,7 +34,7 @@ VARIANTS = {
     "energy_bulk_copies_2_stages": {"CMG_EBULK": "1", "CMG_EBULK_NS": "2"},
     "team_sizes_8_32": {"CMG_FUSE_MASK": "1", "CMG_TS2": "8", "CMG_TS3": "32"},
     "row_parity_levels_2_3": {"CMG_ROWPAIR": "3"},
-    "row_parity_team_sizes_8_8": {"CMG_ROWPAIR": "3", "CMG_TS2": "8", "CMG_TS3": "8"},
+    "row_parity_team_sizes_8_8": {"CMG_ROWPAIR": "3", "CMG_RP_TS2": "8", "CMG_TS3": "8"},
     "row_parity_off": {"CMG_ROWPAIR": "0"},
     "no_programmatic_launch": {"CMG_PDL": "0"},
     "level1_wide_tiles": {"CMG_L1_WIDE": "1"},
