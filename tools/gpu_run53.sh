@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+timeout 1100 python -m pytest tests/test_gpu_variants.py -m gpu -q -x 2>&1 | tail -n 3
+python tools/time_big.py 1024 float64 exact 1 '[{}, {"CMG_L1_RT": "0"}]'
+python tools/time_big.py 4096 float64 exact 1 '[{}, {"CMG_L1_RT": "0"}]'
+python tools/time_big.py 1024 float64 fast 1 '[{"CMG_L1_RT": "1"}, {"CMG_L1_RT": "0"}]'
+for e in '' 'CMG_L1_RT=0'; do env $e python bench.py --steps 5 --warmup 3 --no-cpu --no-fine | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$e', round(d['ms_per_step'],3), d['config']['level_sweep_ms'])"; done
+for e in '' 'CMG_L1_RT=0'; do env $e python bench.py --steps 3 --warmup 3 --no-cpu --no-fine --config 2 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c2 $e', round(d['ms_per_step'],3))"; done
