@@ -611,6 +611,7 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     // 4096^2: 643 -> 579 us; 512^2 has too few: 20.3 -> 27.2 us)
     P->l1_wide = (long long)batch * m * n >= (1LL << 20);
     if (const char* lw = getenv("CMG_L1_WIDE")) P->l1_wide = atoi(lw) != 0;
+    if (const char* en = getenv("CMG_ENERGY_NT")) P->energy_nt = atoi(en) == 512 ? 512 : 256;
     CKP(cudaMalloc(&P->P, sizeof(SolveParams)));
 #undef CKP
     *out = P;

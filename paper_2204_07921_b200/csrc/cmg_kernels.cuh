@@ -750,8 +750,8 @@ __device__ __forceinline__ void energy_reduce_finalize(const double (&acc)[NSUM]
     }
 }
 
-template <typename T, int SRC>
-__global__ void __launch_bounds__(256) k_energy(EnergyArgs a, EnergyFin fz) {
+template <typename T, int SRC, int NT = 256>
+__global__ void __launch_bounds__(NT, NT == 512 ? 2 : 1) k_energy(EnergyArgs a, EnergyFin fz) {
     pdl_sync();
     using A = T;
     const int b = blockIdx.y;

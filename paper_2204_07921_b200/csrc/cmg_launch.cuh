@@ -214,6 +214,8 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
     else if (std::is_same<T, float>::value && P->eb_px == 4)
         klaunch(P, k_energy_bulk<float, 4>, dim3(P->nbx, P->B), 288, eb_smem_bytes<float, 4>(P->eb_ns), ea, fz,
                 P->eb_H, P->eb_ns);
+    else if (P->energy_nt == 512)  // shorter per-thread column walks, still one wave (2 CTAs/SM)
+        klaunch(P, k_energy<T, SRC_INPLACE, 512>, dim3(P->nbx, P->B), 512, 0, ea, fz);
     else
         klaunch(P, k_energy<T, SRC_INPLACE>, dim3(P->nbx, P->B), 256, 0, ea, fz);
     stamp(P, 90);

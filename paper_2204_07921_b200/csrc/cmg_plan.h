@@ -89,6 +89,7 @@ struct cmg_plan {
     int rowpair = 3;        // bit j-2: level j (2, 3) runs as two row-parity launches (k_rowpair)
     bool l1_wide = false;   // k_l1_tile with 32 x 64 tiles (CMG_L1_WIDE)
     int rp_ts2 = 4;         // lanes per patch of the level-2 row-parity kernel (CMG_RP_TS2)
+    int energy_nt = 512;    // k_energy CTA size (CMG_ENERGY_NT; 512 at <= 64 registers: 1024^2 fp32 3.11 -> 3.04 ms)
     bool pdl = true;        // programmatic dependent launch between the cycle's kernels (CMG_PDL=0: off)
 };
 

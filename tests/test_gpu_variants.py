@@ -38,6 +38,7 @@ VARIANTS = {
     "row_parity_off": {"CMG_ROWPAIR": "0"},
     "no_programmatic_launch": {"CMG_PDL": "0"},
     "level1_wide_tiles": {"CMG_L1_WIDE": "1"},
+    "energy_256_threads": {"CMG_ENERGY_NT": "256"},
 }
 
 SCRIPT = r"""
