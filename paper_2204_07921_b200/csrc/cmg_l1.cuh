@@ -254,7 +254,9 @@ __global__ void __launch_bounds__(256) k_l1_tile(FusedArgs<T> a) {
         constexpr int CNT = NI * NK;
         constexpr int ITERS = (CNT + 255) / 256;
         const int single = (a.hc[c] * a.wc[c] == 1);
-#pragma unroll
+        // one copy of the pixel code per colour phase (not per iteration): the
+        // fully unrolled exact kernel overflowed the instruction cache
+#pragma unroll 1
         for (int it = 0; it < ITERS; ++it) {
             const int t = threadIdx.x + it * 256;
             if (CNT % 256 == 0 || it + 1 < ITERS || t < CNT) {
