@@ -264,9 +264,11 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
         if (!P->fused) CK(cudaMemcpyAsync(P->uprev, P->f, bytes, cudaMemcpyDeviceToDevice, P->stream));
         if (P->dtype == CMG_F64) {
             enqueue_fpads<double>(P);
+            enqueue_fsums<double>(P);
             enqueue_energy_ptrs<double>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1, nullptr, 0, -1);
         } else {
             enqueue_fpads<float>(P);
+            enqueue_fsums<float>(P);
             enqueue_energy_ptrs<float>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1, nullptr, 0, -1);
         }
         CK(cudaGetLastError());
@@ -383,7 +385,7 @@ int cmg_plan_destroy(cmg_plan* P) {
     cudaSetDevice(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     if (P->exec) cudaGraphExecDestroy(P->exec);
-    void* ptrs[] = {P->u, P->uprev, P->ubuf[2], P->f, P->ref, P->upad, P->epad, P->partials, P->st, P->ndone, P->eonly, P->raw5, P->P, P->stamps, P->tickets};
+    void* ptrs[] = {P->u, P->uprev, P->ubuf[2], P->f, P->ref, P->upad, P->epad, P->partials, P->st, P->ndone, P->eonly, P->raw5, P->P, P->stamps, P->tickets, P->fsum[2], P->fsum[3]};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 5; ++i)
@@ -530,6 +532,12 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
         CKP(cudaMalloc(&P->upad, P->esz * maxpad * batch));
         P->upad_elems = maxpad;
     }
+    // per-patch f sums for the fast mean path of levels 2-3 (f* without f pixels)
+    if (const char* fs = getenv("CMG_FSUM")) P->use_fsum = atoi(fs) != 0;
+    if (P->use_fsum && mode == CMG_MODE_MEAN && P->prec == CMG_PREC_FAST)
+        for (int j = 2; j <= std::min(layers, 3); ++j)
+            if (!P->lv[j].general)
+                CKP(cudaMalloc(&P->fsum[j], sizeof(double) * (size_t)P->lv[j].mj * P->lv[j].nj * batch));
     P->egeneral = !(single_chunk(m, 1) && single_chunk(n, 1));
     P->eH = m + 2;
     P->eW = n + 2;
@@ -688,9 +696,11 @@ int cmg_sweep_layer(cmg_plan* P, void* u_host, const void* f_host, int layer, do
         result = P->ubuf[2];
     } else if (P->dtype == CMG_F64) {
         enqueue_fpads<double>(P);
+        enqueue_fsums<double>(P);
         for (int c = 0; c < 4; ++c) enqueue_sweep<double>(P, layer, c);
     } else {
         enqueue_fpads<float>(P);
+        enqueue_fsums<float>(P);
         for (int c = 0; c < 4; ++c) enqueue_sweep<float>(P, layer, c);
     }
     CK(cudaGetLastError());
@@ -918,11 +928,14 @@ int cmg_buffer_upload(cmg_plan* P, int index, const void* host) {
     void* p = buffer_ptr(P, index);
     if (!p) return fail(CMG_EINVAL, "buffer index must be 0..4");
     CK(cudaMemcpyAsync(p, host, P->esz * (size_t)P->N * P->B, cudaMemcpyHostToDevice, P->stream));
-    if (index == 3) {  // f changed: refresh the padded f of general levels
-        if (P->dtype == CMG_F64)
+    if (index == 3) {  // f changed: refresh the padded f of general levels and the patch sums of f
+        if (P->dtype == CMG_F64) {
             enqueue_fpads<double>(P);
-        else
+            enqueue_fsums<double>(P);
+        } else {
             enqueue_fpads<float>(P);
+            enqueue_fsums<float>(P);
+        }
     }
     CK(cudaStreamSynchronize(P->stream));
     return CMG_OK;

@@ -74,6 +74,11 @@ struct SweepArgs {
     ImgState* st;
     int dbg;  // diagnostics: bit0 skip planes, bit1 skip f*, bit2 skip apply, bit3 exit early
     BackK bk;
+    // fast mean mode: per-patch sums of the padded f of this level ([B][mj][nj], fp64, computed once
+    // per solve by k_patch_fsum), so f* = (sum f - sum u) / S^2 needs no f pixels; nullptr: unused
+    const double* fsum;
+    long long fs_img;
+    int fs_ld;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -286,9 +291,40 @@ __device__ __forceinline__ ArgBest<T> arg_reduce(ArgBest<T> x) {
     return x;
 }
 
+// fast mean mode: closed-form c_half of a patch, planes split
+// over the TS lanes, then the backward steps
+template <typename T, int LAYER, int TS, class Acc>
+__device__ __forceinline__ T patch_chalf_fast_team(const Acc& U, int ci, int cc, int lane, T fstar,
+                                                   const SweepArgs<T>& a) {
+    constexpr int NPL = 1 << (LAYER + 2);
+    constexpr int NPAIR = NPL / 2;
+    constexpr unsigned FULL = 0xffffffffu;
+    const T uo = U(ci, cc);
+    T part = T(0);
+#pragma unroll
+    for (int k = 0; k < (NPAIR + TS - 1) / TS; ++k) {
+        const int pi = lane + k * TS;
+        if (pi < NPAIR) {
+            const PlaneRT pl = PlaneRT::getg(2 * pi);
+            const int Lq = pl.x0 * pl.x0 + pl.x1 * pl.x1;
+            const T up = U(ci + pl.x0, cc + pl.x1), um = U(ci - pl.x0, cc - pl.x1);
+            const T uq = U(ci + pl.y0, cc + pl.y1), umq = U(ci - pl.y0, cc - pl.y1);
+            const T sp = up + um;
+            const T N = sp - T(2) * uo;
+            const T Dd = up - um;
+            const T base = Dd * Dd + T(4 * Lq);
+            const T Sa = sp - T(2) * uq, Sb = sp - T(2) * umq;
+            part += (sqrt(T(Lq)) * N) * (frsqrt(Sa * Sa + base) + frsqrt(Sb * Sb + base));
+        }
+    }
+#pragma unroll
+    for (int o = TS / 2; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o, TS);
+    return backward_steps<T, LAYER, PREC_FAST>(part * T(1.0 / NPL), fstar, a);
+}
+
 template <typename T, int LAYER, int MODE, int PREC, int TS, class Acc, class AccF = Acc>
 __device__ __forceinline__ T patch_solve_team(const Acc& U, const AccF& F, int R0, int C0, int lane,
-                                              const SweepArgs<T>& a) {
+                                              const SweepArgs<T>& a, const double* fsum_patch = nullptr) {
     using O = X<T>;
     constexpr int S = (1 << LAYER) - 1;
     constexpr int R = 1 << (LAYER - 1);
@@ -297,6 +333,20 @@ __device__ __forceinline__ T patch_solve_team(const Acc& U, const AccF& F, int R
     static_assert(TS >= S && TS <= 32 && (32 % TS) == 0, "team size");
     const int ci = R0 + R - 1, cc = C0 + R - 1;
     auto D = [&](int aa, int bb) { return O::sub(F(R0 + aa, C0 + bb), U(R0 + aa, C0 + bb)); };
+
+    if constexpr (MODE == MODE_MEAN && PREC == PREC_FAST) {
+        if (fsum_patch) {  // f* = (sum f - sum u) / S^2 with the precomputed sum of f (fast mode only)
+            T ur = T(0);
+            if (lane < S) {
+#pragma unroll
+                for (int bb = 0; bb < S; ++bb) ur += U(R0 + lane, C0 + bb);
+            }
+#pragma unroll
+            for (int o = TS / 2; o > 0; o >>= 1) ur += __shfl_xor_sync(FULL, ur, o, TS);
+            const T fstar = T((__ldg(fsum_patch) - (double)ur) * (1.0 / (S * S)));
+            return patch_chalf_fast_team<T, LAYER, TS>(U, ci, cc, lane, fstar, a);
+        }
+    }
 
     // f*: lane t owns row t (driver.py:244-246; rows sequential, each pairwise)
     T rowsum = T(0);
@@ -387,9 +437,9 @@ __device__ __forceinline__ T patch_solve_team(const Acc& U, const AccF& F, int R
 
 template <typename T, int LAYER, int MODE, int PREC, int TS>
 __device__ __forceinline__ T patch_solve_team_border(const T* u, const T* f, int R0, int C0, int lane,
-                                                  const SweepArgs<T>& a) {
+                                                  const SweepArgs<T>& a, const double* fsp = nullptr) {
     Reflect<T> U{u, a.m, a.n}, F{f, a.m, a.n};
-    return patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, a);
+    return patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, a, fsp);
 }
 
 template <typename T, int LAYER, int MODE, int PREC, int SRC, int TS>
@@ -413,12 +463,14 @@ __global__ void __launch_bounds__(256) k_sweep_team(SweepArgs<T> a) {
         Padded<T> U{a.upad + (long long)b * a.pstride, a.W}, F{a.fpad + (long long)b * a.pstride, a.W};
         c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, a);
     } else {
+        const double* fsp =
+            a.fsum ? a.fsum + (long long)b * a.fs_img + (long long)(R0 / S) * a.fs_ld + C0 / S : nullptr;
         const bool inside = (R0 >= 1) && (C0 >= 1) && (R0 + S < a.m) && (C0 + S < a.n);
         if (__all_sync(0xffffffffu, inside)) {
             Direct<T> U{u, a.n}, F{f, a.n};
-            c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, a);
+            c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, a, fsp);
         } else {
-            c = patch_solve_team_border<T, LAYER, MODE, PREC, TS>(u, f, R0, C0, lane, a);
+            c = patch_solve_team_border<T, LAYER, MODE, PREC, TS>(u, f, R0, C0, lane, a, fsp);
         }
     }
     if (!valid || (a.dbg & 4)) return;
@@ -828,6 +880,23 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 1) k_energy(EnergyArgs a, 
         }
     }
     energy_reduce_finalize(acc, a, fz, b);
+}
+
+// Per-patch sums of the odd-padded f of one level (fast mean mode: f* =
+// (sum f - sum u) / S^2, f is constant through a solve).  One thread per patch.
+template <typename T, int S>
+__global__ void k_patch_fsum(const T* __restrict__ f, double* out, int m, int n, int mj, int nj, long long istride) {
+    pdl_sync();
+    const int b = blockIdx.y;
+    const long long np = (long long)mj * nj;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= np) return;
+    const int pr = (int)(e / nj), pc = (int)(e % nj);
+    const Reflect<T> F{f + (long long)b * istride, m, n};
+    double acc = 0.0;
+    for (int i = 0; i < S; ++i)
+        for (int k = 0; k < S; ++k) acc += (double)F(pr * S + i, pc * S + k);
+    out[(long long)b * np + e] = acc;
 }
 
 // ---------------------------------------------------------------------------

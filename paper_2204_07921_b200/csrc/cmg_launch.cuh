@@ -108,7 +108,26 @@ SweepArgs<T> make_sweep_args(const cmg_plan* P, int layer, int color) {
     a.bk.w0 = P->hostP.w[layer][0];
     a.bk.den0 = P->hostP.den[layer][0];
     a.bk.inv0 = 1.0 / P->hostP.den[layer][0];
+    a.fsum = (layer <= 3) ? P->fsum[layer] : nullptr;
+    a.fs_img = (long long)L.mj * L.nj;
+    a.fs_ld = L.nj;
     return a;
+}
+
+// per-patch f sums of levels 2-3 (fast mean mode): after every change of f
+template <typename T>
+void enqueue_fsums(cmg_plan* P) {
+    for (int j = 2; j <= std::min(P->layers, 3); ++j) {
+        if (!P->fsum[j]) continue;
+        const Level& L = P->lv[j];
+        const long long np = (long long)L.mj * L.nj;
+        const dim3 grd((unsigned)((np + 255) / 256), P->B);
+        if (j == 2)
+            klaunch(P, k_patch_fsum<T, 3>, grd, 256, 0, (const T*)P->f, P->fsum[j], P->m, P->n, L.mj, L.nj, P->N);
+        else
+            klaunch(P, k_patch_fsum<T, 7>, grd, 256, 0, (const T*)P->f, P->fsum[j], P->m, P->n, L.mj, L.nj, P->N);
+        P->enq += 1;
+    }
 }
 
 template <typename T>
@@ -750,6 +769,7 @@ int energy_bulk_cfg_impl(int batch, int m, int n, int px, int ns, int* H_out) {
     template void cmg::enqueue_energy<T>(cmg_plan*, bool, double*, int);            \
     template void cmg::enqueue_copy_prev<T>(cmg_plan*);                             \
     template void cmg::enqueue_fpads<T>(cmg_plan*);                             \
+    template void cmg::enqueue_fsums<T>(cmg_plan*);                             \
     template cudaError_t cmg::persist_launch<T>(cmg_plan*, bool, int);               \
     template void cmg::enqueue_fused_level<T>(cmg_plan*, int, const void*, void*);  \
     template void cmg::enqueue_energy_ptrs<T>(cmg_plan*, const void*, const void*, bool, double*, int, double*, \

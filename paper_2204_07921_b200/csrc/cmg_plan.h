@@ -90,6 +90,8 @@ struct cmg_plan {
     bool l1_wide = false;   // k_l1_tile with 32 x 64 tiles (CMG_L1_WIDE)
     int rp_ts2 = 4;         // lanes per patch of the level-2 row-parity kernel (CMG_RP_TS2)
     int energy_nt = 512;    // k_energy CTA size (CMG_ENERGY_NT; 512 at <= 64 registers: 1024^2 fp32 3.11 -> 3.04 ms)
+    double* fsum[4] = {nullptr, nullptr, nullptr, nullptr};  // [level] per-patch f sums (fast mean, levels 2-3)
+    bool use_fsum = true;   // CMG_FSUM=0: f* from f pixels as in exact mode
     bool pdl = true;        // programmatic dependent launch between the cycle's kernels (CMG_PDL=0: off)
 };
 
@@ -137,6 +139,8 @@ template <typename T>
 void enqueue_copy_prev(cmg_plan* P);
 template <typename T>
 void enqueue_fpads(cmg_plan* P);
+template <typename T>
+void enqueue_fsums(cmg_plan* P);
 template <typename T>
 cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full);
 template <typename T>

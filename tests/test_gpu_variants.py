@@ -125,6 +125,7 @@ VARIANTS32_EXACT = {
 VARIANTS32_CLOSE = {
     "fused_all": {"CMG_FUSE_MASK": "7"},
     "per_colour_only": {"CMG_FUSED": "0"},
+    "per_colour_f_pixels": {"CMG_FUSED": "0", "CMG_FSUM": "0"},
 }
 
 
