@@ -130,11 +130,18 @@ struct PlaneLin {
 // ---- one patch, TS == 1 (compile-time offsets) ---------------------------
 template <typename T, int LAYER, int MODE, int PREC, class Acc>
 __device__ __forceinline__ T coarse_solve_thread(const Acc& U, const Acc& F, const SweepArgs<T>& a, T w, T den,
-                                                 T inv) {
+                                                 T inv, const double* fsp = nullptr) {
     using O = X<T>;
     constexpr int S = (1 << LAYER) - 1, R = 1 << (LAYER - 1), NPL = 1 << (LAYER + 2);
     T acc;
-    if (a.flat) {
+    if (MODE == MODE_MEAN && PREC == PREC_FAST && fsp) {  // f* from the precomputed sum of f (fast mode)
+        T us = T(0);
+#pragma unroll
+        for (int aa = 0; aa < S; ++aa)
+#pragma unroll
+            for (int bb = 0; bb < S; ++bb) us += U(aa, bb);
+        acc = T(__ldg(fsp) - (double)us);
+    } else if (a.flat) {
         acc = fstar_flat_sum<T, S>(U, F, 0, 0);
     } else {
         acc = T(0);
@@ -329,9 +336,11 @@ __device__ __forceinline__ T coarse_solve_team(const T* su, const T* sf, int bas
     return c;
 }
 
-template <typename T, int LAYER, int MODE, int PREC, int TP, int TS, int NT>
+// FS: fast mean mode with per-patch f sums (a.fsum): f is not staged at all
+template <typename T, int LAYER, int MODE, int PREC, int TP, int TS, int NT, bool FS = false>
 __global__ void __launch_bounds__(NT) k_coarse_tile(FusedArgs<T> a, const __grid_constant__ CUtensorMap tmu,
                                                     const __grid_constant__ CUtensorMap tmf, int use_tma) {
+    static_assert(!FS || (TS == 1 && MODE == MODE_MEAN && PREC == PREC_FAST), "f sums: one thread per patch, fast");
     pdl_sync();
     using G = CoarseGeom<T, LAYER, TP>;
     constexpr int S = G::S, RD = G::RD, LD = G::LD;
@@ -340,7 +349,7 @@ __global__ void __launch_bounds__(NT) k_coarse_tile(FusedArgs<T> a, const __grid
     unsigned char* base128 = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
     T* su_al = reinterpret_cast<T*>(base128);
     T* sf_al = su_al + G::CELLS_AL;
-    PlaneLin* tab = reinterpret_cast<PlaneLin*>(sf_al + G::CELLS_AL);
+    PlaneLin* tab = reinterpret_cast<PlaneLin*>(su_al + (FS ? 1 : 2) * G::CELLS_AL);
     unsigned long long* mbarp = reinterpret_cast<unsigned long long*>(tab + G::NPL + (G::NPL & 1));
     const int b = blockIdx.z;
     const int P0 = blockIdx.y * TP, Q0 = blockIdx.x * TP;
@@ -383,9 +392,9 @@ __global__ void __launch_bounds__(NT) k_coarse_tile(FusedArgs<T> a, const __grid
         if (threadIdx.x == 0) mbar_init(mbarp, 1);
         __syncthreads();
         if (threadIdx.x == 0) {
-            mbar_expect_tx(mbarp, 2u * RD * G::BW * (unsigned)sizeof(T));
+            mbar_expect_tx(mbarp, (FS ? 1u : 2u) * RD * G::BW * (unsigned)sizeof(T));
             tma_load_3d(su_al, &tmu, c0 - sh, r0, b, mbarp);
-            tma_load_3d(sf_al, &tmf, c0 - sh, r0, b, mbarp);
+            if (!FS) tma_load_3d(sf_al, &tmf, c0 - sh, r0, b, mbarp);
         }
         mbar_wait(mbarp, 0);
     } else {
@@ -399,7 +408,7 @@ __global__ void __launch_bounds__(NT) k_coarse_tile(FusedArgs<T> a, const __grid
                 const int gk = c0 + k;
                 if (gk >= 0 && gk < n) {
                     su[i * LD + k] = ur[gk];
-                    sf[i * LD + k] = fr[gk];
+                    if (!FS) sf[i * LD + k] = fr[gk];
                 }
             }
         }
@@ -424,7 +433,7 @@ __global__ void __launch_bounds__(NT) k_coarse_tile(FusedArgs<T> a, const __grid
     bool bad = false;
     // pad values of u are refreshed after every phase on border tiles; f's once
     if (border) {
-        coarse_fill_pad<T, LAYER, TP>(sf, r0, c0, m, n, mp, np);
+        if (!FS) coarse_fill_pad<T, LAYER, TP>(sf, r0, c0, m, n, mp, np);
         coarse_fill_pad<T, LAYER, TP>(su, r0, c0, m, n, mp, np);
     }
     static_for<0, 4>([&](auto cphase) {
@@ -459,7 +468,8 @@ __global__ void __launch_bounds__(NT) k_coarse_tile(FusedArgs<T> a, const __grid
             T cv;
             if constexpr (TS == 1) {
                 SBase<T, LD> U{su, base}, F{sf, base};
-                if (valid) cv = coarse_solve_thread<T, LAYER, MODE, PREC>(U, F, sa, w, den, inv);
+                const double* fsp = FS ? a.fsum + b * a.fs_img + (long long)pa * a.fs_ld + pb : nullptr;
+                if (valid) cv = coarse_solve_thread<T, LAYER, MODE, PREC>(U, F, sa, w, den, inv, fsp);
             } else {
                 cv = coarse_solve_team<T, LAYER, MODE, PREC, TS>(su, sf, base, lane, tab, LD, sa, w, den, inv);
             }

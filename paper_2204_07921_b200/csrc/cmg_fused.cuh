@@ -59,6 +59,9 @@ struct FusedArgs {
     float nz;     // -0.0f, opaque to the compiler (k_l1_x2 products)
     const SolveParams* P;
     ImgState* st;
+    const double* fsum;  // fast mean: per-patch sums of f of this level (k_patch_fsum) or nullptr
+    long long fs_img;
+    int fs_ld;
 };
 
 template <int LAYER, int TP>

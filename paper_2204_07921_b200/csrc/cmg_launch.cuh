@@ -395,12 +395,12 @@ struct CoarseCfg<double, 3> {
     static constexpr int TP = 4, TS = 8, NT = 128;
 };
 
-template <typename T, int LAYER, int MODE, int PREC>
-void launch_coarse(cmg_plan* P, const FusedArgs<T>& a) {
+template <typename T, int LAYER, int MODE, int PREC, bool FS>
+void launch_coarse_v(cmg_plan* P, const FusedArgs<T>& a) {
     using C = CoarseCfg<T, LAYER>;
     using G = CoarseGeom<T, LAYER, C::TP>;
-    const size_t smem = 128 + 2 * sizeof(T) * G::CELLS_AL + sizeof(PlaneLin) * (G::NPL + 2) + 16;
-    auto kern = k_coarse_tile<T, LAYER, MODE, PREC, C::TP, C::TS, C::NT>;
+    const size_t smem = 128 + (FS ? 1 : 2) * sizeof(T) * G::CELLS_AL + sizeof(PlaneLin) * (G::NPL + 2) + 16;
+    auto kern = k_coarse_tile<T, LAYER, MODE, PREC, C::TP, C::TS, C::NT, FS>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -416,6 +416,18 @@ void launch_coarse(cmg_plan* P, const FusedArgs<T>& a) {
     memset(&dummy, 0, sizeof(dummy));
     klaunch(P, kern, grd, C::NT, smem, a, tma ? P->tmap[LAYER][bi] : dummy, tma ? P->tmap[LAYER][3] : dummy,
                                           tma ? 1 : 0);
+}
+
+template <typename T, int LAYER, int MODE, int PREC>
+void launch_coarse(cmg_plan* P, const FusedArgs<T>& a) {
+    using C = CoarseCfg<T, LAYER>;
+    if constexpr (C::TS == 1 && MODE == MODE_MEAN && PREC == PREC_FAST) {
+        if (a.fsum) {  // per-patch f sums: u only in shared memory
+            launch_coarse_v<T, LAYER, MODE, PREC, true>(P, a);
+            return;
+        }
+    }
+    launch_coarse_v<T, LAYER, MODE, PREC, false>(P, a);
 }
 
 // encoded as box_width * 4096 + box_height
@@ -533,6 +545,9 @@ void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
     }
     a.P = P->P;
     a.st = P->st;
+    a.fsum = (layer >= 2 && layer <= 3) ? P->fsum[layer] : nullptr;
+    a.fs_img = (long long)L.mj * L.nj;
+    a.fs_ld = L.nj;
     if (P->mode == CMG_MODE_GAUSS)
         dispatch_fused<T, MODE_GAUSS, PREC_EXACT>(P, layer, a);
     else if (P->prec == CMG_PREC_FAST)
