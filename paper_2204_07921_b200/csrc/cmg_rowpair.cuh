@@ -103,17 +103,32 @@ __device__ __forceinline__ void rp_stage(const RowPairArgs<T>& a, const RPItem<T
     const int m = a.c0.m, n = a.c0.n, p = a.c0.p;
     T* fwin = win + G::ROWS * G::WIN;
     const int wlo = max(it.wk0, 0), whi = min(it.wk0 + G::WIN, n);  // in-image window columns
+    // per column: every row's load is issued before the first shared-memory store
+    // (one global round trip per column instead of one per row)
+    constexpr int NR = G::ROWS + S;  // u rows R0-1 .. R0+S, then f rows R0 .. R0+S-1
+    const T* srow[G::ROWS];
 #pragma unroll
     for (int ri = 0; ri < G::ROWS; ++ri) {
         const int i = it.wr0 + ri;
-        if (i < 0 || i >= m) continue;
-        const T* srow = rp_src_row<T, S>(it, p, i) + (long long)i * n;
-        const T* frow = it.f + (long long)i * n;
-        for (int k = wlo + threadIdx.x; k < whi; k += G::NT) {
-            T* du = win + ri * G::WIN + (k - it.wk0);
-            T* df = fwin + (ri - 1) * G::WIN + (k - it.wk0);
-            *du = srow[k];
-            if (ri >= 1 && ri <= S) *df = __ldg(frow + k);
+        srow[ri] = rp_src_row<T, S>(it, p, i) + (long long)i * n;
+    }
+    const T* frow0 = it.f + (long long)it.R0 * n;
+    for (int k = wlo + threadIdx.x; k < whi; k += G::NT) {
+        T v[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const int i = (r < G::ROWS) ? it.wr0 + r : it.R0 + (r - G::ROWS);
+            if (i >= 0 && i < m) v[r] = (r < G::ROWS) ? srow[r][k] : __ldg(frow0 + (long long)(r - G::ROWS) * n + k);
+        }
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const int i = (r < G::ROWS) ? it.wr0 + r : it.R0 + (r - G::ROWS);
+            if (i >= 0 && i < m) {
+                if (r < G::ROWS)
+                    win[r * G::WIN + (k - it.wk0)] = v[r];
+                else
+                    fwin[(r - G::ROWS) * G::WIN + (k - it.wk0)] = v[r];
+            }
         }
     }
 }
