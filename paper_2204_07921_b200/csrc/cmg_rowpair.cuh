@@ -113,17 +113,19 @@ __device__ __forceinline__ void rp_stage(const RowPairArgs<T>& a, const RPItem<T
         srow[ri] = rp_src_row<T, S>(it, p, i) + (long long)i * n;
     }
     const T* frow0 = it.f + (long long)it.R0 * n;
+    const int nr = a.c0.fsum ? G::ROWS : NR;  // fast mean with per-patch f sums: no f pixels needed
     for (int k = wlo + threadIdx.x; k < whi; k += G::NT) {
         T v[NR];
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
             const int i = (r < G::ROWS) ? it.wr0 + r : it.R0 + (r - G::ROWS);
-            if (i >= 0 && i < m) v[r] = (r < G::ROWS) ? srow[r][k] : __ldg(frow0 + (long long)(r - G::ROWS) * n + k);
+            if (r < nr && i >= 0 && i < m)
+                v[r] = (r < G::ROWS) ? srow[r][k] : __ldg(frow0 + (long long)(r - G::ROWS) * n + k);
         }
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
             const int i = (r < G::ROWS) ? it.wr0 + r : it.R0 + (r - G::ROWS);
-            if (i >= 0 && i < m) {
+            if (r < nr && i >= 0 && i < m) {
                 if (r < G::ROWS)
                     win[r * G::WIN + (k - it.wk0)] = v[r];
                 else
@@ -146,7 +148,7 @@ __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem
     T* fwin = win + G::ROWS * G::WIN;
     const int wlo = max(wk0, 0), whi = min(wk0 + G::WIN, n);
     const int kmax = A0.W - 2;  // np (padded columns run -1 .. np)
-    if (it.border) {  // padded f cells of the patch row (f is constant: reflect from global)
+    if (it.border && !A0.fsum) {  // padded f cells of the patch row (f is constant: reflect from global)
         const Reflect<T> FR{it.f, m, n};
         for (int e = threadIdx.x; e < S * G::WIN; e += G::NT) {
             const int ri = e / G::WIN, ck = e % G::WIN;
@@ -202,7 +204,9 @@ __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem
         if (__any_sync(0xffffffffu, active)) {
             const int Jc = active ? J : J0;  // inactive teams shadow a valid patch (converged shuffles)
             const int C0 = Jc * S;
-            const T c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, A);
+            const double* fsp =
+                A.fsum ? A.fsum + (long long)it.b * A.fs_img + (long long)(R0 / S) * A.fs_ld + Jc : nullptr;
+            const T c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, A, fsp);
             if (active) {
                 if (lane == 0 && !isfinite(c)) bad = true;
                 for (int e = lane; e < S * S; e += TS) {
