@@ -166,6 +166,12 @@ int build_graph(cmg_plan* P, int full, bool has_ref) {
         }
     }
     P->nodes_per_cycle = P->enq;
+    if (P->launch_err != cudaSuccess) {
+        const cudaError_t le = P->launch_err;
+        P->launch_err = cudaSuccess;
+        cudaGraphDestroy(g);
+        return fail(CMG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(le));
+    }
     cudaError_t ie = cudaGraphInstantiate(&P->exec, g, 0);
     cudaGraphDestroy(g);
     if (ie != cudaSuccess) return fail(CMG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
@@ -272,6 +278,11 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
             enqueue_energy_ptrs<float>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1, nullptr, 0, -1);
         }
         CK(cudaGetLastError());
+        if (P->launch_err != cudaSuccess) {
+            const cudaError_t le = P->launch_err;
+            P->launch_err = cudaSuccess;
+            return fail(CMG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(le));
+        }
         init_launches = P->enq;
         if (P->use_while) {
             CK(cudaGraphLaunch(P->exec, P->stream));

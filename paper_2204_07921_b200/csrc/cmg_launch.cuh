@@ -298,11 +298,7 @@ void launch_fused(cmg_plan* P, const FusedArgs<T>& a) {
     constexpr int RD = FusedGeom<LAYER, TP>::RD;
     const size_t smem = 2 * sizeof(T) * RD * RD;
     auto kern = k_level_fused<T, LAYER, MODE, PREC, TP, TS>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
+    smem_attr(kern, smem);
     const Level& L = P->lv[LAYER];
     FusedArgs<T> b = a;
     const int tiles_r = (L.mj + TP - 1) / TP;
@@ -329,7 +325,7 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
                 constexpr int TH = decltype(th)::value, TW = decltype(tw)::value;
                 using G = L1Geom<float, TH, TW>;
                 const size_t smem = sizeof(float) * (2 + 8 * G::PLANE);
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                smem_attr(kern, smem);
                 const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
                 klaunch(P, kern, grd, nt, smem, a);
             };
@@ -356,11 +352,7 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
         using G = L1Geom<T, TH, TW>;
         const size_t smem = 2 * sizeof(T) * 4 * G::PLANE;
         auto kern = k_l1_tile<T, MODE, PREC, TH, TW>;
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr_set = true;
-        }
+        smem_attr(kern, smem);
         const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
         klaunch(P, kern, grd, 256, smem, a);
     };
@@ -401,11 +393,7 @@ void launch_coarse_v(cmg_plan* P, const FusedArgs<T>& a) {
     using G = CoarseGeom<T, LAYER, C::TP>;
     const size_t smem = 128 + (FS ? 1 : 2) * sizeof(T) * G::CELLS_AL + sizeof(PlaneLin) * (G::NPL + 2) + 16;
     auto kern = k_coarse_tile<T, LAYER, MODE, PREC, C::TP, C::TS, C::NT, FS>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
+    smem_attr(kern, smem);
     const Level& L = P->lv[LAYER];
     const dim3 grd((L.nj + C::TP - 1) / C::TP, (L.mj + C::TP - 1) / C::TP, P->B);
     int bi = -1;
@@ -451,11 +439,7 @@ void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
     r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
     const size_t smem = sizeof(T) * (G::ROWS + G::S) * G::WIN;  // u window + f of the patch row
     auto kern = k_rowpair<T, LAYER, MODE, PREC, TS>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
+    smem_attr(kern, smem);
     for (int p = 0; p < 2; ++p) {
         const int rows = (L.mj - p + 1) / 2;
         if (rows <= 0) continue;
@@ -710,12 +694,13 @@ void coop_launch_v(cmg_plan* P, void* u, const int* seq, int nseq) {
     a.P = P->P;
     a.st = P->st;
     const size_t smem = 16 * ((P->B * sizeof(int) + 15) / 16) + sizeof(T) * (64 + 256 + 2);
-    static int grid = 0;  // per instantiation (one device per process in practice)
-    if (grid == 0) {
-        int nb = 0, dev = 0, nsm = 0;
+    // grid sized per plan and device: occupancy depends on the batch-sized
+    // dynamic shared memory and on the device the plan lives on
+    int grid = 0;
+    {
+        int nb = 0, nsm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 256, smem);
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P->device);
         grid = nsm * std::max(1, std::min(nb, P->coop_occ));
     }
     cudaLaunchConfig_t cfg;
@@ -729,7 +714,8 @@ void coop_launch_v(cmg_plan* P, void* u, const int* seq, int nseq) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, a);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+    if (e != cudaSuccess && P->launch_err == cudaSuccess) P->launch_err = e;
     P->enq += 1;
 }
 

@@ -6,6 +6,9 @@
 #include <cstring>
 #include <utility>
 #include <cuda_runtime.h>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "../../include/cmg.h"
 #include "cmg_kernels.cuh"
@@ -63,6 +66,7 @@ struct cmg_plan {
     bool coarse_tile = true;  // k_coarse_tile for fused levels 2-3
     bool coop = false;        // cooperative kernel for runs of non-fused coarse levels
     int coop_occ = 4;         // max CTAs per SM of that kernel
+    cudaError_t launch_err = cudaSuccess;  // first failed checked launch (cooperative path)
     bool tma_ok[4] = {false, false, false, false};
     CUtensorMap tmap[4][4];  // [level][buffer 0..2 = u rotation, 3 = f]  // fused L2/L3 tile variants (FusedCfg)  // dedicated level-1 tile kernel (k_l1_tile) instead of k_level_fused<1>  // diagnostics bits (CMG_DBG), see SweepArgs::dbg  // team sizes (lanes per patch) of levels 2 and 3
     // graphs
@@ -113,6 +117,23 @@ inline void klaunch(const cmg_plan* P, void (*kern)(KP...), dim3 grid, dim3 bloc
     cfg.attrs = at;
     cfg.numAttrs = P->pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// opt a kernel into its dynamic shared memory on the CURRENT device, once per
+// (kernel, device): function attributes are per device, so a process with
+// plans on several GPUs needs them set on each
+inline void smem_attr_raw(const void* kern, size_t smem) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (done.insert({kern, dev}).second)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+template <typename... KP>
+inline void smem_attr(void (*kern)(KP...), size_t smem) {
+    smem_attr_raw((const void*)kern, smem);
 }
 
 // diagnostics: a 1-thread kernel that appends %globaltimer to a device buffer

@@ -191,21 +191,36 @@ def rel_err_u(u_new: np.ndarray, u_old: np.ndarray) -> float:
 # ---------------------------------------------------------------------------
 # plan cache (device buffers and CUDA graphs are reused across calls)
 # ---------------------------------------------------------------------------
-_plans: dict = {}
-_plans_lock = threading.Lock()
+_tls = threading.local()
+_PLAN_CAP = 16
 
 
 def get_plan(m: int, n: int, batch: int, cfg: SolverConfig) -> N.Plan:
-    key = (threading.get_ident(), m, n, batch, cfg.layers, cfg.mode, cfg.dtype, cfg.precision, cfg.device)
-    with _plans_lock:
-        p = _plans.get(key)
-        if p is None:
-            if len(_plans) >= 16:
-                for k in list(_plans)[:8]:
-                    _plans.pop(k).close()
-            p = N.Plan(m, n, batch, cfg.layers, cfg.mode, cfg.dtype, cfg.precision, cfg.device)
-            _plans[key] = p
+    """Per-thread plan cache: a plan (device buffers, stream, graph) is only
+    ever used and evicted by the thread that created it, so one thread's
+    eviction can never free a plan another thread is solving with."""
+    plans = getattr(_tls, "plans", None)
+    if plans is None:
+        plans = _tls.plans = {}
+    key = (m, n, batch, cfg.layers, cfg.mode, cfg.dtype, cfg.precision, cfg.device)
+    p = plans.get(key)
+    if p is None:
+        if len(plans) >= _PLAN_CAP:
+            for k in list(plans)[: _PLAN_CAP // 2]:
+                plans.pop(k).close()
+        p = N.Plan(m, n, batch, cfg.layers, cfg.mode, cfg.dtype, cfg.precision, cfg.device)
+        plans[key] = p
     return p
+
+
+def _as_image(x, what: str) -> Image:
+    """Duck-typed Image: ours, the reference's ``curvemg.image.Image`` or any
+    object with a 2-D ``.data`` and a ``.peak`` (image.py:34-75)."""
+    if isinstance(x, Image):
+        return x
+    if hasattr(x, "data") and hasattr(x, "peak"):
+        return Image(np.asarray(x.data), float(x.peak))
+    raise TypeError(f"{what} must be an Image")
 
 
 def _np_dtype(cfg: SolverConfig):
@@ -262,8 +277,9 @@ def denoise(f: Image, config, reference: Image | None = None) -> tuple[Image, Co
     SolverDivergence when the objective becomes non-finite.
     """
     cfg = _coerce_config(config)
-    if not isinstance(f, Image):
-        raise TypeError("f must be an Image")
+    f = _as_image(f, "f")
+    if reference is not None:
+        reference = _as_image(reference, "reference")
     if reference is not None and reference.shape != f.shape:
         raise ValueError(f"shape mismatch: {f.shape} vs {reference.shape}")
     m, n = f.shape

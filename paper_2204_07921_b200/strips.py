@@ -205,6 +205,11 @@ class LocalExchange:
         for src, dst, lo, hi in self.pairs:
             d = self.strips[dst].rows(index, lo, hi)
             d.copy_(self.strips[src].rows(index, lo, hi))
+        # the copies run on torch's stream; libcmg's plan streams are
+        # non-blocking, so the next level step must not start before they land
+        for s in self.strips:
+            if hasattr(s, "sync"):
+                s.sync()
 
     def allreduce(self, v: np.ndarray) -> np.ndarray:
         return v
