@@ -474,7 +474,16 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     // fp64 fast 3.92 vs 3.75; configs 1 / 2: 2.69 -> 2.61 ms, 18.7 -> 18.1 ms with row pairs)
     P->rowpair = small_job ? 3 : 0;
     P->rp_ts2 = 4;
+    // large fast-mean jobs: level 3 as row-parity launches with one thread per
+    // patch (per-patch f sums, u-only windows): one read and one write of u per
+    // level instead of four per-colour passes
+    const bool fast_mean = mode == CMG_MODE_MEAN && P->prec == CMG_PREC_FAST;
+    if (!small_job && fast_mean && layers >= 3) {
+        P->rowpair |= 2;
+        P->rp1 |= 2;
+    }
     if (const char* rp = getenv("CMG_ROWPAIR")) P->rowpair = atoi(rp) & 3;
+    if (const char* r1 = getenv("CMG_RP1")) P->rp1 = atoi(r1) & 3;
     if (const char* rt = getenv("CMG_RP_TS2")) P->rp_ts2 = atoi(rt);
     if (layers >= 2 && (P->rowpair & 1)) P->fuse_mask |= 2;
     if (layers >= 3 && (P->rowpair & 2)) P->fuse_mask |= 4;

@@ -330,16 +330,20 @@ __device__ __forceinline__ T patch_solve_team(const Acc& U, const AccF& F, int R
     constexpr int R = 1 << (LAYER - 1);
     constexpr int NPL = 1 << (LAYER + 2);
     constexpr unsigned FULL = 0xffffffffu;
-    static_assert(TS >= S && TS <= 32 && (32 % TS) == 0, "team size");
+    // teams narrower than a patch row only exist for the fast mean mode with
+    // per-patch f sums (large-job row-parity kernel, one thread per patch)
+    static_assert(TS <= 32 && (32 % TS) == 0, "team size");
+    static_assert(TS >= S || (MODE == MODE_MEAN && PREC == PREC_FAST), "team narrower than a patch row");
     const int ci = R0 + R - 1, cc = C0 + R - 1;
     auto D = [&](int aa, int bb) { return O::sub(F(R0 + aa, C0 + bb), U(R0 + aa, C0 + bb)); };
 
     if constexpr (MODE == MODE_MEAN && PREC == PREC_FAST) {
-        if (fsum_patch) {  // f* = (sum f - sum u) / S^2 with the precomputed sum of f (fast mode only)
+        if (TS < S || fsum_patch) {  // f* = (sum f - sum u) / S^2 with the precomputed sum of f (fast mode only)
             T ur = T(0);
-            if (lane < S) {
 #pragma unroll
-                for (int bb = 0; bb < S; ++bb) ur += U(R0 + lane, C0 + bb);
+            for (int r = lane; r < S; r += TS) {
+#pragma unroll
+                for (int bb = 0; bb < S; ++bb) ur += U(R0 + r, C0 + bb);
             }
 #pragma unroll
             for (int o = TS / 2; o > 0; o >>= 1) ur += __shfl_xor_sync(FULL, ur, o, TS);
@@ -347,6 +351,9 @@ __device__ __forceinline__ T patch_solve_team(const Acc& U, const AccF& F, int R
             return patch_chalf_fast_team<T, LAYER, TS>(U, ci, cc, lane, fstar, a);
         }
     }
+    if constexpr (TS < S) {
+        return T(0);  // unreachable: TS < S implies the f-sum branch above
+    } else {
 
     // f*: lane t owns row t (driver.py:244-246; rows sequential, each pairwise)
     T rowsum = T(0);
@@ -433,6 +440,7 @@ __device__ __forceinline__ T patch_solve_team(const Acc& U, const AccF& F, int R
         chalf = __shfl_sync(FULL, ph, 0, TS);
     }
     return backward_steps<T, LAYER, PREC>(chalf, fstar, a);
+    }
 }
 
 template <typename T, int LAYER, int MODE, int PREC, int TS>

@@ -428,17 +428,19 @@ inline int coarse_region_impl(int layer) {
 
 // levels 2-3: two launches (patch-row parity 0, then 1), each running its two
 // colours in a shared-memory window (cmg_rowpair.cuh); X -> Y
-template <typename T, int LAYER, int MODE, int PREC, int TS>
+template <typename T, int LAYER, int MODE, int PREC, int TS, int NT = 256>
 void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
-    using G = RowPairGeom<LAYER, TS>;
+    using G = RowPairGeom<LAYER, TS, NT>;
     const Level& L = P->lv[LAYER];
     RowPairArgs<T> r;
     r.X = X;
     r.Y = Y;
     r.nj = L.nj;
     r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
-    const size_t smem = sizeof(T) * (G::ROWS + G::S) * G::WIN;  // u window + f of the patch row
-    auto kern = k_rowpair<T, LAYER, MODE, PREC, TS>;
+    // u window + f of the patch row (no f rows with per-patch f sums)
+    const bool fs = P->fsum[LAYER] != nullptr && MODE == MODE_MEAN && PREC == PREC_FAST;
+    const size_t smem = sizeof(T) * (G::ROWS + (fs ? 0 : G::S)) * G::WIN;
+    auto kern = k_rowpair<T, LAYER, MODE, PREC, TS, NT>;
     smem_attr(kern, smem);
     for (int p = 0; p < 2; ++p) {
         const int rows = (L.mj - p + 1) / 2;
@@ -456,6 +458,18 @@ void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
 
 template <typename T, int MODE, int PREC>
 void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
+    // one thread per patch (fast mean with per-patch f sums; large jobs): a
+    // ~64 KB window of one patch row per CTA
+    if constexpr (MODE == MODE_MEAN && PREC == PREC_FAST) {
+        if (((P->rp1 >> (layer - 2)) & 1) && a.fsum) {
+            constexpr int NT1 = sizeof(T) == 4 ? 128 : 64;
+            if (layer == 2)
+                launch_rowpair<T, 2, MODE, PREC, 1, NT1>(P, a.uin, a.uout);
+            else
+                launch_rowpair<T, 3, MODE, PREC, 1, NT1>(P, a.uin, a.uout);
+            return;
+        }
+    }
     // team sizes: level 2 {4, 8} lanes per patch (P->rp_ts2), level 3 {8, 16}
     if (layer == 2) {
         if (P->rp_ts2 >= 8)

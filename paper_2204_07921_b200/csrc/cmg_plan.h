@@ -93,6 +93,7 @@ struct cmg_plan {
     int rowpair = 3;        // bit j-2: level j (2, 3) runs as two row-parity launches (k_rowpair)
     bool l1_wide = false;   // k_l1_tile with 32 x 64 tiles (CMG_L1_WIDE)
     int rp_ts2 = 4;         // lanes per patch of the level-2 row-parity kernel (CMG_RP_TS2)
+    int rp1 = 0;            // bit j-2: level j's row-parity kernel runs one thread per patch (CMG_RP1)
     int energy_nt = 512;    // k_energy CTA size (CMG_ENERGY_NT; 512 at <= 64 registers: 1024^2 fp32 3.11 -> 3.04 ms)
     double* fsum[4] = {nullptr, nullptr, nullptr, nullptr};  // [level] per-patch f sums (fast mean, levels 2-3)
     bool use_fsum = true;   // CMG_FSUM=0: f* from f pixels as in exact mode

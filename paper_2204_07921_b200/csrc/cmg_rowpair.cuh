@@ -45,10 +45,10 @@ struct WinAcc {
     __device__ __forceinline__ T operator()(int i, int k) const { return s[(i - r0) * ld + (k - k0)]; }
 };
 
-template <int LAYER, int TS>
+template <int LAYER, int TS, int NT_ = 256>
 struct RowPairGeom {
     static constexpr int S = (1 << LAYER) - 1;
-    static constexpr int NT = 256;
+    static constexpr int NT = NT_;
     static constexpr int TEAMS = NT / TS;
     static constexpr int TPC = 2 * TEAMS - 2;          // owned patch columns per CTA (even)
     static constexpr int WIN = (TPC + 2) * S + 2;      // window columns: [(J0-1)S-1, (J0+TPC+1)S]
@@ -64,9 +64,9 @@ struct RPItem {
     T* Yb;
 };
 
-template <typename T, int LAYER, int TS>
+template <typename T, int LAYER, int TS, int NT>
 __device__ __forceinline__ RPItem<T> rp_item(const RowPairArgs<T>& a, int b, int pr, int tile) {
-    using G = RowPairGeom<LAYER, TS>;
+    using G = RowPairGeom<LAYER, TS, NT>;
     constexpr int S = G::S;
     const SweepArgs<T>& A0 = a.c0;
     const int m = A0.m, n = A0.n;
@@ -96,9 +96,9 @@ __device__ __forceinline__ const T* rp_src_row(const RPItem<T>& it, int p, int i
 
 // stage the in-image cells of an item's window: u rows R0-1 .. R0+S into win,
 // f rows R0 .. R0+S-1 into fwin = win + ROWS*WIN.
-template <typename T, int LAYER, int TS>
+template <typename T, int LAYER, int TS, int NT>
 __device__ __forceinline__ void rp_stage(const RowPairArgs<T>& a, const RPItem<T>& it, T* win) {
-    using G = RowPairGeom<LAYER, TS>;
+    using G = RowPairGeom<LAYER, TS, NT>;
     constexpr int S = G::S;
     const int m = a.c0.m, n = a.c0.n, p = a.c0.p;
     T* fwin = win + G::ROWS * G::WIN;
@@ -138,9 +138,9 @@ __device__ __forceinline__ void rp_stage(const RowPairArgs<T>& a, const RPItem<T
 // everything after staging: border refills, the two colours, write-back.
 // Starts and ends with the window consistent across the CTA (callers sync
 // before; this ends with a barrier-free write-back of owned pixels).
-template <typename T, int LAYER, int MODE, int PREC, int TS>
+template <typename T, int LAYER, int MODE, int PREC, int TS, int NT>
 __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem<T>& it, T* win) {
-    using G = RowPairGeom<LAYER, TS>;
+    using G = RowPairGeom<LAYER, TS, NT>;
     constexpr int S = G::S;
     const SweepArgs<T>& A0 = a.c0;
     const int m = A0.m, n = A0.n, p = A0.p;
@@ -229,9 +229,9 @@ __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem
 }
 
 // stopped image: carry the owned pixels along the buffer rotation
-template <typename T, int LAYER, int TS>
+template <typename T, int LAYER, int TS, int NT>
 __device__ __forceinline__ void rp_copy_owned(const RowPairArgs<T>& a, const RPItem<T>& it) {
-    using G = RowPairGeom<LAYER, TS>;
+    using G = RowPairGeom<LAYER, TS, NT>;
     const int n = a.c0.n;
     for (int i = it.R0; i < it.orow1; ++i)
         for (int k = it.ok0 + threadIdx.x; k < it.ok1; k += G::NT) {
@@ -240,19 +240,19 @@ __device__ __forceinline__ void rp_copy_owned(const RowPairArgs<T>& a, const RPI
         }
 }
 
-template <typename T, int LAYER, int MODE, int PREC, int TS>
-__global__ void __launch_bounds__(256) k_rowpair(RowPairArgs<T> a) {
+template <typename T, int LAYER, int MODE, int PREC, int TS, int NT = 256>
+__global__ void __launch_bounds__(NT) k_rowpair(RowPairArgs<T> a) {
     pdl_sync();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* win = reinterpret_cast<T*>(smem_raw);
-    const RPItem<T> it = rp_item<T, LAYER, TS>(a, blockIdx.z, blockIdx.y, blockIdx.x);
+    const RPItem<T> it = rp_item<T, LAYER, TS, NT>(a, blockIdx.z, blockIdx.y, blockIdx.x);
     if (a.c0.st[it.b].done) {
-        rp_copy_owned<T, LAYER, TS>(a, it);
+        rp_copy_owned<T, LAYER, TS, NT>(a, it);
         return;
     }
-    rp_stage<T, LAYER, TS>(a, it, win);
+    rp_stage<T, LAYER, TS, NT>(a, it, win);
     __syncthreads();
-    rp_compute<T, LAYER, MODE, PREC, TS>(a, it, win);
+    rp_compute<T, LAYER, MODE, PREC, TS, NT>(a, it, win);
 }
 
 }  // namespace cmg
