@@ -348,6 +348,12 @@ __device__ __forceinline__ T patch_solve_team(const Acc& U, const AccF& F, int R
 #pragma unroll
             for (int o = TS / 2; o > 0; o >>= 1) ur += __shfl_xor_sync(FULL, ur, o, TS);
             const T fstar = T((__ldg(fsum_patch) - (double)ur) * (1.0 / (S * S)));
+            if constexpr (TS == 1) {  // one thread per patch: compile-time plane offsets
+                const T uo = U(ci, cc);
+                T sum = T(0);
+                static_for<0, NPL / 2>([&](auto k) { sum += pair_fast<T, decltype(k)::value>(U, ci, cc, uo); });
+                return backward_steps<T, LAYER, PREC_FAST>(sum * T(1.0 / NPL), fstar, a);
+            }
             return patch_chalf_fast_team<T, LAYER, TS>(U, ci, cc, lane, fstar, a);
         }
     }

@@ -456,6 +456,38 @@ void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
     }
 }
 
+// persistent bulk-copy variant (one thread per patch, fast mean + f sums)
+template <typename T, int LAYER, int NT>
+void launch_rowpair_bulk(cmg_plan* P, const T* X, T* Y) {
+    using G = RowPairGeom<LAYER, 1, NT, 16 / (int)sizeof(T)>;
+    const Level& L = P->lv[LAYER];
+    RowPairArgs<T> r;
+    r.X = X;
+    r.Y = Y;
+    r.nj = L.nj;
+    r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
+    const size_t smem = 2 * sizeof(T) * G::ROWS * G::WIN;
+    auto kern = k_rowpair_bulk<T, LAYER, NT>;
+    smem_attr(kern, smem);
+    int occ = 1, nsm = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P->device);
+    for (int p = 0; p < 2; ++p) {
+        const int rows = (L.mj - p + 1) / 2;
+        if (rows <= 0) continue;
+        r.c0 = make_sweep_args<T>(P, LAYER, 2 * p);
+        r.c1 = make_sweep_args<T>(P, LAYER, 2 * p + 1);
+        const long long items = (long long)rows * r.ntiles * P->B;
+        const int grid = (int)std::min<long long>(items, (long long)nsm * std::max(1, occ));
+        klaunch(P, kern, dim3(grid), NT, smem, r, rows, P->B);
+        if (p == 0) {
+            stamp(P, 10 * LAYER + 8);
+        } else {
+            P->enq += 1;  // the caller counts one launch per level
+        }
+    }
+}
+
 template <typename T, int MODE, int PREC>
 void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
     // one thread per patch (fast mean with per-patch f sums; large jobs): a
@@ -463,6 +495,19 @@ void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
     if constexpr (MODE == MODE_MEAN && PREC == PREC_FAST) {
         if (((P->rp1 >> (layer - 2)) & 1) && a.fsum) {
             constexpr int NT1 = sizeof(T) == 4 ? 128 : 64;
+            if (P->rp_bulk && ((size_t)P->n * sizeof(T)) % 16 == 0) {
+                if (sizeof(T) == 4 && P->rp_nt == 64) {
+                    if (layer == 2)
+                        launch_rowpair_bulk<T, 2, 64>(P, a.uin, a.uout);
+                    else
+                        launch_rowpair_bulk<T, 3, 64>(P, a.uin, a.uout);
+                } else if (layer == 2) {
+                    launch_rowpair_bulk<T, 2, NT1>(P, a.uin, a.uout);
+                } else {
+                    launch_rowpair_bulk<T, 3, NT1>(P, a.uin, a.uout);
+                }
+                return;
+            }
             if (layer == 2)
                 launch_rowpair<T, 2, MODE, PREC, 1, NT1>(P, a.uin, a.uout);
             else

@@ -25,6 +25,7 @@
 #pragma once
 
 #include "cmg_kernels.cuh"
+#include "cmg_coarse.cuh"
 
 namespace cmg {
 
@@ -45,13 +46,17 @@ struct WinAcc {
     __device__ __forceinline__ T operator()(int i, int k) const { return s[(i - r0) * ld + (k - k0)]; }
 };
 
-template <int LAYER, int TS, int NT_ = 256>
+template <int LAYER, int TS, int NT_ = 256, int A_ = 1>
 struct RowPairGeom {
     static constexpr int S = (1 << LAYER) - 1;
     static constexpr int NT = NT_;
     static constexpr int TEAMS = NT / TS;
     static constexpr int TPC = 2 * TEAMS - 2;          // owned patch columns per CTA (even)
-    static constexpr int WIN = (TPC + 2) * S + 2;      // window columns: [(J0-1)S-1, (J0+TPC+1)S]
+    // window columns: [(J0-1)S-1, (J0+TPC+1)S]; with A_ > 1 the window origin is
+    // floored to a multiple of A_ elements (16-byte aligned bulk copies) and the
+    // width padded to a multiple of A_ that still covers the shifted window
+    static constexpr int WIN0 = (TPC + 2) * S + 2;
+    static constexpr int WIN = A_ == 1 ? WIN0 : ((WIN0 + 2 * (A_ - 1)) / A_) * A_;
     static constexpr int ROWS = S + 2;                 // window rows: [R0-1, R0+S]
 };
 
@@ -138,9 +143,9 @@ __device__ __forceinline__ void rp_stage(const RowPairArgs<T>& a, const RPItem<T
 // everything after staging: border refills, the two colours, write-back.
 // Starts and ends with the window consistent across the CTA (callers sync
 // before; this ends with a barrier-free write-back of owned pixels).
-template <typename T, int LAYER, int MODE, int PREC, int TS, int NT>
+template <typename T, int LAYER, int MODE, int PREC, int TS, int NT, int A = 1>
 __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem<T>& it, T* win) {
-    using G = RowPairGeom<LAYER, TS, NT>;
+    using G = RowPairGeom<LAYER, TS, NT, A>;
     constexpr int S = G::S;
     const SweepArgs<T>& A0 = a.c0;
     const int m = A0.m, n = A0.n, p = A0.p;
@@ -253,6 +258,80 @@ __global__ void __launch_bounds__(NT) k_rowpair(RowPairArgs<T> a) {
     rp_stage<T, LAYER, TS, NT>(a, it, win);
     __syncthreads();
     rp_compute<T, LAYER, MODE, PREC, TS, NT>(a, it, win);
+}
+
+// ---------------------------------------------------------------------------
+// Large jobs, fast mean mode with per-patch f sums: the same row-parity
+// launches, one thread per patch, as a PERSISTENT kernel whose windows are
+// streamed by bulk asynchronous copies (cp.async.bulk + mbarrier, one copy per
+// window row) into two shared-memory stages: item i+1's rows are in flight
+// while item i computes.  u only (no f pixels).  Requires n*sizeof(T) % 16 == 0.
+// ---------------------------------------------------------------------------
+template <typename T, int LAYER, int NT>
+__global__ void __launch_bounds__(NT) k_rowpair_bulk(RowPairArgs<T> a, int rows, int B) {
+    pdl_sync();
+    constexpr int A = 16 / (int)sizeof(T);
+    using G = RowPairGeom<LAYER, 1, NT, A>;
+    constexpr int STAGE = G::ROWS * G::WIN;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* stage0 = reinterpret_cast<T*>(smem_raw);
+    __shared__ __align__(8) unsigned long long full[2];
+    const int tid = threadIdx.x;
+    const int m = a.c0.m, n = a.c0.n, p = a.c0.p;
+    const long long per_img = (long long)rows * a.ntiles;
+    const long long items = per_img * B;
+    auto item_of = [&](long long itx) {
+        const int b = (int)(itx / per_img);
+        const long long r = itx - (long long)b * per_img;
+        const int pr = (int)(r / a.ntiles), tile = (int)(r - (long long)pr * a.ntiles);
+        RPItem<T> x = rp_item<T, LAYER, 1, NT>(a, b, pr, tile);
+        x.wk0 = (x.wk0 >= 0) ? (x.wk0 / A) * A : -(((-x.wk0) + A - 1) / A) * A;
+        x.border = (x.wr0 < 0) || (x.wr0 + G::ROWS > m) || (x.wk0 < 0) || (x.wk0 + G::WIN > n);
+        return x;
+    };
+    // thread 0: one bulk copy per in-image window row (16-byte aligned ends)
+    auto issue = [&](const RPItem<T>& x, T* win, unsigned long long* bar) {
+        if (a.c0.st[x.b].done) {
+            mbar_expect_tx(bar, 0u);
+            return;
+        }
+        const int wlo = max(x.wk0, 0), whi = min(x.wk0 + G::WIN, n);
+        const unsigned bytes = (unsigned)(whi - wlo) * (unsigned)sizeof(T);
+        int nrow = 0;
+#pragma unroll
+        for (int ri = 0; ri < G::ROWS; ++ri) {
+            const int i = x.wr0 + ri;
+            nrow += (i >= 0 && i < m) ? 1 : 0;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes of the previous item
+        mbar_expect_tx(bar, bytes * (unsigned)nrow);
+#pragma unroll
+        for (int ri = 0; ri < G::ROWS; ++ri) {
+            const int i = x.wr0 + ri;
+            if (i >= 0 && i < m)
+                bulk_g2s(win + ri * G::WIN + (wlo - x.wk0), rp_src_row<T, G::S>(x, p, i) + (long long)i * n + wlo, bytes,
+                         bar);
+        }
+    };
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+    }
+    __syncthreads();
+    long long itx = blockIdx.x;
+    if (tid == 0 && itx < items) issue(item_of(itx), stage0, &full[0]);
+    for (int i = 0; itx < items; itx += gridDim.x, ++i) {
+        const RPItem<T> cur = item_of(itx);
+        const long long nx = itx + gridDim.x;
+        if (tid == 0 && nx < items) issue(item_of(nx), stage0 + ((i + 1) & 1) * STAGE, &full[(i + 1) & 1]);
+        mbar_wait(&full[i & 1], (unsigned)((i >> 1) & 1));
+        if (a.c0.st[cur.b].done) {
+            rp_copy_owned<T, LAYER, 1, NT>(a, cur);
+        } else {
+            rp_compute<T, LAYER, MODE_MEAN, PREC_FAST, 1, NT, A>(a, cur, stage0 + (i & 1) * STAGE);
+        }
+        __syncthreads();  // stage (i & 1) is refilled by the copy issued in iteration i + 1
+    }
 }
 
 }  // namespace cmg
