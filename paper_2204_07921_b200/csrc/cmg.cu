@@ -478,7 +478,10 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     // patch (per-patch f sums, u-only windows): one read and one write of u per
     // level instead of four per-colour passes
     const bool fast_mean = mode == CMG_MODE_MEAN && P->prec == CMG_PREC_FAST;
-    if (!small_job && fast_mean && layers >= 3) {
+    // (wide images only: a 512-wide image leaves most of a ~900-column window
+    // empty; config 4's 64 x 512^2 stays on the per-colour team kernels,
+    // 111 vs 265 us per level-3 visit)
+    if (!small_job && fast_mean && layers >= 3 && n >= 2048) {
         P->rowpair |= 2;
         P->rp1 |= 2;
     }

@@ -494,13 +494,18 @@ void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
     // ~64 KB window of one patch row per CTA
     if constexpr (MODE == MODE_MEAN && PREC == PREC_FAST) {
         if (((P->rp1 >> (layer - 2)) & 1) && a.fsum) {
-            constexpr int NT1 = sizeof(T) == 4 ? 128 : 64;
+            constexpr int NT1 = 64;
             if (P->rp_bulk && ((size_t)P->n * sizeof(T)) % 16 == 0) {
-                if (sizeof(T) == 4 && P->rp_nt == 64) {
+                if (sizeof(T) == 4 && P->rp_nt == 128) {
                     if (layer == 2)
-                        launch_rowpair_bulk<T, 2, 64>(P, a.uin, a.uout);
+                        launch_rowpair_bulk<T, 2, 128>(P, a.uin, a.uout);
                     else
-                        launch_rowpair_bulk<T, 3, 64>(P, a.uin, a.uout);
+                        launch_rowpair_bulk<T, 3, 128>(P, a.uin, a.uout);
+                } else if (P->rp_nt == 32) {
+                    if (layer == 2)
+                        launch_rowpair_bulk<T, 2, 32>(P, a.uin, a.uout);
+                    else
+                        launch_rowpair_bulk<T, 3, 32>(P, a.uin, a.uout);
                 } else if (layer == 2) {
                     launch_rowpair_bulk<T, 2, NT1>(P, a.uin, a.uout);
                 } else {

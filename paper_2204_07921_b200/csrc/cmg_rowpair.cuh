@@ -214,10 +214,16 @@ __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem
             const T c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, A, fsp);
             if (active) {
                 if (lane == 0 && !isfinite(c)) bad = true;
-                for (int e = lane; e < S * S; e += TS) {
-                    const int i = R0 + e / S, k = C0 + e % S;
-                    if (i < m && k < n) {
-                        T* px = win + (i - wr0) * G::WIN + (k - wk0);
+                // prolongation u += c on the patch's in-image pixels (hierarchy.py:117-126);
+                // the element loop has a compile-time trip count (e / S, e % S fold for TS = 1)
+                T* base = win + (R0 - wr0) * G::WIN + (C0 - wk0);
+                const int rmax = min(S, m - R0), cmax = min(S, n - C0);
+#pragma unroll
+                for (int t = 0; t < (S * S + TS - 1) / TS; ++t) {
+                    const int e = lane + t * TS;
+                    const int r = e / S, k = e - (e / S) * S;
+                    if (e < S * S && r < rmax && k < cmax) {
+                        T* px = base + r * G::WIN + k;
                         *px = X<T>::add(*px, c);
                     }
                 }
