@@ -457,8 +457,8 @@ void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
 }
 
 // persistent bulk-copy variant (one thread per patch, fast mean + f sums)
-template <typename T, int LAYER, int NT>
-void launch_rowpair_bulk(cmg_plan* P, const T* X, T* Y) {
+template <typename T, int LAYER, int NT, int STAGES>
+void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y) {
     using G = RowPairGeom<LAYER, 1, NT, 16 / (int)sizeof(T)>;
     const Level& L = P->lv[LAYER];
     RowPairArgs<T> r;
@@ -466,8 +466,8 @@ void launch_rowpair_bulk(cmg_plan* P, const T* X, T* Y) {
     r.Y = Y;
     r.nj = L.nj;
     r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
-    const size_t smem = 2 * sizeof(T) * G::ROWS * G::WIN;
-    auto kern = k_rowpair_bulk<T, LAYER, NT>;
+    const size_t smem = STAGES * sizeof(T) * G::ROWS * G::WIN;
+    auto kern = k_rowpair_bulk<T, LAYER, NT, STAGES>;
     smem_attr(kern, smem);
     int occ = 1, nsm = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
@@ -486,6 +486,14 @@ void launch_rowpair_bulk(cmg_plan* P, const T* X, T* Y) {
             P->enq += 1;  // the caller counts one launch per level
         }
     }
+}
+
+template <typename T, int LAYER, int NT>
+void launch_rowpair_bulk(cmg_plan* P, const T* X, T* Y) {
+    if (P->rp_stages == 1)
+        launch_rowpair_bulk_s<T, LAYER, NT, 1>(P, X, Y);
+    else
+        launch_rowpair_bulk_s<T, LAYER, NT, 2>(P, X, Y);
 }
 
 template <typename T, int MODE, int PREC>

@@ -95,6 +95,7 @@ struct cmg_plan {
     int rp_ts2 = 4;         // lanes per patch of the level-2 row-parity kernel (CMG_RP_TS2)
     int rp1 = 0;            // bit j-2: level j's row-parity kernel runs one thread per patch (CMG_RP1)
     int rp_bulk = 1;        // ... as the persistent bulk-copy kernel (CMG_RP_BULK)
+    int rp_stages = 1;      // shared-memory stages of that kernel (CMG_RP_STAGES: 1 or 2; 1 = more CTAs per SM, faster)
     int rp_nt = 64;         // threads per CTA of that kernel (CMG_RP_NT: 32, 64 or 128 [fp32])
     int energy_nt = 512;    // k_energy CTA size (CMG_ENERGY_NT; 512 at <= 64 registers: 1024^2 fp32 3.11 -> 3.04 ms)
     double* fsum[4] = {nullptr, nullptr, nullptr, nullptr};  // [level] per-patch f sums (fast mean, levels 2-3)

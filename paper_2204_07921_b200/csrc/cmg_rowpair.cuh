@@ -143,7 +143,9 @@ __device__ __forceinline__ void rp_stage(const RowPairArgs<T>& a, const RPItem<T
 // everything after staging: border refills, the two colours, write-back.
 // Starts and ends with the window consistent across the CTA (callers sync
 // before; this ends with a barrier-free write-back of owned pixels).
-template <typename T, int LAYER, int MODE, int PREC, int TS, int NT, int A = 1>
+// EDGES_ONLY: the caller bulk-stores the A-aligned interior of each owned row;
+// the threads write only the (< A) unaligned columns at both ends
+template <typename T, int LAYER, int MODE, int PREC, int TS, int NT, int A = 1, bool EDGES_ONLY = false>
 __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem<T>& it, T* win) {
     using G = RowPairGeom<LAYER, TS, NT, A>;
     constexpr int S = G::S;
@@ -234,10 +236,30 @@ __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem
     });
     if (bad) A0.st[it.b].bad = 1;
     // owned pixels -> Y
-    for (int i = R0; i < it.orow1; ++i)
-        for (int k = it.ok0 + threadIdx.x; k < it.ok1; k += G::NT)
+    if constexpr (EDGES_ONLY) {
+        const int a0 = min(((it.ok0 + A - 1) / A) * A, it.ok1), a1 = max((it.ok1 / A) * A, a0);
+        const int nl = a0 - it.ok0, ne = nl + (it.ok1 - a1);
+        const int rows = it.orow1 - R0;
+        for (int e = threadIdx.x; e < rows * ne; e += G::NT) {
+            const int i = R0 + e / ne, j = e % ne;
+            const int k = j < nl ? it.ok0 + j : a1 + (j - nl);
             it.Yb[(long long)i * n + k] = win[(i - wr0) * G::WIN + (k - wk0)];
+        }
+    } else {
+        for (int i = R0; i < it.orow1; ++i)
+            for (int k = it.ok0 + threadIdx.x; k < it.ok1; k += G::NT)
+                it.Yb[(long long)i * n + k] = win[(i - wr0) * G::WIN + (k - wk0)];
+    }
 }
+
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // stopped image: carry the owned pixels along the buffer rotation
 template <typename T, int LAYER, int TS, int NT>
@@ -273,7 +295,7 @@ __global__ void __launch_bounds__(NT) k_rowpair(RowPairArgs<T> a) {
 // window row) into two shared-memory stages: item i+1's rows are in flight
 // while item i computes.  u only (no f pixels).  Requires n*sizeof(T) % 16 == 0.
 // ---------------------------------------------------------------------------
-template <typename T, int LAYER, int NT>
+template <typename T, int LAYER, int NT, int STAGES>
 __global__ void __launch_bounds__(NT) k_rowpair_bulk(RowPairArgs<T> a, int rows, int B) {
     pdl_sync();
     constexpr int A = 16 / (int)sizeof(T);
@@ -281,7 +303,7 @@ __global__ void __launch_bounds__(NT) k_rowpair_bulk(RowPairArgs<T> a, int rows,
     constexpr int STAGE = G::ROWS * G::WIN;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* stage0 = reinterpret_cast<T*>(smem_raw);
-    __shared__ __align__(8) unsigned long long full[2];
+    __shared__ __align__(8) unsigned long long full[STAGES];
     const int tid = threadIdx.x;
     const int m = a.c0.m, n = a.c0.n, p = a.c0.p;
     const long long per_img = (long long)rows * a.ntiles;
@@ -295,8 +317,10 @@ __global__ void __launch_bounds__(NT) k_rowpair_bulk(RowPairArgs<T> a, int rows,
         x.border = (x.wr0 < 0) || (x.wr0 + G::ROWS > m) || (x.wk0 < 0) || (x.wk0 + G::WIN > n);
         return x;
     };
-    // thread 0: one bulk copy per in-image window row (16-byte aligned ends)
+    // thread 0: one bulk copy per in-image window row (16-byte aligned ends);
+    // the stage's pending bulk stores must have read it first
     auto issue = [&](const RPItem<T>& x, T* win, unsigned long long* bar) {
+        bulk_wait_read0();
         if (a.c0.st[x.b].done) {
             mbar_expect_tx(bar, 0u);
             return;
@@ -319,25 +343,45 @@ __global__ void __launch_bounds__(NT) k_rowpair_bulk(RowPairArgs<T> a, int rows,
                          bar);
         }
     };
-    if (tid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-    }
+    // thread 0: bulk stores of the A-aligned interior of the owned rows (the
+    // threads wrote the unaligned ends); smem column k and global column k share
+    // their 16-byte phase because the window origin is A-aligned
+    auto store = [&](const RPItem<T>& x, const T* win) {
+        const int a0 = min(((x.ok0 + A - 1) / A) * A, x.ok1), a1 = max((x.ok1 / A) * A, a0);
+        if (a1 <= a0) return;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int i = x.R0; i < x.orow1; ++i)
+            bulk_s2g(x.Yb + (long long)i * n + a0, win + (i - x.wr0) * G::WIN + (a0 - x.wk0),
+                     (unsigned)(a1 - a0) * (unsigned)sizeof(T));
+        bulk_commit();
+    };
+    if (tid == 0)
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
     __syncthreads();
     long long itx = blockIdx.x;
-    if (tid == 0 && itx < items) issue(item_of(itx), stage0, &full[0]);
+    if (STAGES > 1 && tid == 0 && itx < items) issue(item_of(itx), stage0, &full[0]);
     for (int i = 0; itx < items; itx += gridDim.x, ++i) {
         const RPItem<T> cur = item_of(itx);
-        const long long nx = itx + gridDim.x;
-        if (tid == 0 && nx < items) issue(item_of(nx), stage0 + ((i + 1) & 1) * STAGE, &full[(i + 1) & 1]);
-        mbar_wait(&full[i & 1], (unsigned)((i >> 1) & 1));
+        const int st = i % STAGES;
+        if (tid == 0) {
+            if (STAGES == 1) {
+                issue(cur, stage0, &full[0]);
+            } else {
+                const long long nx = itx + gridDim.x;
+                if (nx < items) issue(item_of(nx), stage0 + ((i + 1) % STAGES) * STAGE, &full[(i + 1) % STAGES]);
+            }
+        }
+        mbar_wait(&full[st], (unsigned)((i / STAGES) & 1));
+        T* win = stage0 + st * STAGE;
         if (a.c0.st[cur.b].done) {
             rp_copy_owned<T, LAYER, 1, NT>(a, cur);
         } else {
-            rp_compute<T, LAYER, MODE_MEAN, PREC_FAST, 1, NT, A>(a, cur, stage0 + (i & 1) * STAGE);
+            rp_compute<T, LAYER, MODE_MEAN, PREC_FAST, 1, NT, A, true>(a, cur, win);
+            if (tid == 0) store(cur, win);
         }
-        __syncthreads();  // stage (i & 1) is refilled by the copy issued in iteration i + 1
+        __syncthreads();  // the stage is refilled by a later iteration's copy
     }
+    if (tid == 0) bulk_wait0();
 }
 
 }  // namespace cmg
