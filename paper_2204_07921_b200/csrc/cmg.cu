@@ -478,13 +478,19 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     // patch (per-patch f sums, u-only windows): one read and one write of u per
     // level instead of four per-colour passes
     const bool fast_mean = mode == CMG_MODE_MEAN && P->prec == CMG_PREC_FAST;
-    // (wide images only: a 512-wide image leaves most of a ~900-column window
-    // empty; config 4's 64 x 512^2 stays on the per-colour team kernels,
-    // 111 vs 265 us per level-3 visit)
+    // (B200, round 2: 16384^2 level 3 1.37 -> 0.44 ms, level 2 0.89 -> 0.65 ms vs the
+    // fused coarse tile; 64 x 512^2 level 2 133 -> 87 us with 32-thread CTAs.  Level 3
+    // only on wide images: a 512-wide image leaves most of the window empty and
+    // config 4 keeps the per-colour team kernels there, 111 vs 153 us)
+    if (!small_job && fast_mean && layers >= 2 && n >= 256) {
+        P->rowpair |= 1;
+        P->rp1 |= 1;
+    }
     if (!small_job && fast_mean && layers >= 3 && n >= 2048) {
         P->rowpair |= 2;
         P->rp1 |= 2;
     }
+    P->rp_nt = n >= 2048 ? 64 : 32;
     if (const char* rp = getenv("CMG_ROWPAIR")) P->rowpair = atoi(rp) & 3;
     if (const char* r1 = getenv("CMG_RP1")) P->rp1 = atoi(r1) & 3;
     if (const char* rb = getenv("CMG_RP_BULK")) P->rp_bulk = atoi(rb);
