@@ -147,6 +147,18 @@ def workload(cfgid: int, dtype: str, prec: str):
     return c, size, layers, eps, batch, f"config{cfgid}: {desc}, alpha=0.06, {dtype}, precision={prec}"
 
 
+def config_dict(cfgid: int, desc: str, images: int, cycles: int, parallelism: str) -> dict:
+    """The `config` object both arms print (same keys -> same_config)."""
+    return {"workload": desc, "images": images, "cycles": cycles, "parallelism": parallelism,
+            "l2": "flushed (512 MiB write) before every timed step; a 1024^2 solve is L2-resident after its "
+                  "first sweep" if cfgid != 5 else "flushed before every step; the 16384^2 image (1 GiB per "
+                  "buffer) is far larger than L2"}
+
+
+WORKLOAD_IMAGES = {1: 1, 2: 1, 3: 1, 4: 64, 5: 1}
+WORKLOAD_CYCLES = {1: 10, 2: 50, 3: 40, 4: 20, 5: 10}  # config 2 stops at its tolerance (<= 50)
+
+
 def cpu_workload(cfgid: int, fp32: bool):
     """The bounded CPU sample of a config: the config's own solve (same
     stopping rule and cycle cap) on image 0, except config 5 whose 16384^2
@@ -199,6 +211,8 @@ def run_reference(args):
     value = float(np.mean(vals))
     sample = (f"one solve per step of {f.shape[0]}x{f.shape[1]} ({desc}; {its} cycles); oracle/cmg_oracle.c "
               f"(C restatement of the reference NumPy algorithm, fp64), OpenMP over patches, {threads} threads")
+    par = {3: "replicas", 4: "dp (images sharded)", 5: "strips"}.get(args.config, "replicas")
+    par = f"{par} x{ws}" if ws > 1 else ("single GPU, batch 64" if args.config == 4 else "single GPU")
     line = {
         "impl": "reference",
         "metric": "Mpixel-sweeps/s",
@@ -209,11 +223,11 @@ def run_reference(args):
         "warmup": args.warmup,
         "ms_per_step": 1e3 * float(np.mean(times)),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if args.config != 5 else "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (BASELINE seeded generator, SURVEY 8d)",
-        "config": {"workload": desc, "sample": sample},
+        "config": config_dict(args.config, desc, WORKLOAD_IMAGES[args.config], its, par),
         "cpu_baseline": {"value": value, "unit": "Mpixel-sweeps/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "Mpixel-sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -384,10 +398,8 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64" if args.dtype == "float64" else "f32",
         "data": "synthetic (BASELINE seeded generator, SURVEY 8d)",
-        "config": {"workload": desc, "images": imgs_total, "cycles": cycles, "time_to_tolerance_ms": value_ms,
-                   "l2": "flushed (512 MiB write) before every timed step; a 1024^2 solve is L2-resident after "
-                         "its first sweep",
-                   "parallelism": parallelism, **extra},
+        "config": config_dict(args.config, desc, imgs_total, cycles, parallelism),
+        "detail": {"time_to_tolerance_ms": value_ms, **extra},
         "e2e": {"value": e2e_value, "unit": "Mpixel-sweeps/s", "h2d_bytes_per_step": int(nbytes_in),
                 "d2h_bytes_per_step": int(nbytes_out), "ms_per_step": e2e_ms,
                 "path": "cmg_solve (C ABI) with pinned host buffers"},
@@ -397,14 +409,35 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": int(alg_bytes), "launch_ms": l1_ms, "peak_source": peak_src},
         "clocks": clocks,
     }
+    # L2-resident working set (u, f, the rotation buffers of a <= ~32 MB job):
+    # the level-1 sweep is measured against the L2 read bandwidth of this GPU,
+    # measured live (cmg_l2_read_bandwidth: 32 MiB streamed 50 times)
+    if 4 * esz * m_loc * n * (len(idx) if args.config == 4 else 1) <= (64 << 20):
+        l2 = N.l2_read_bandwidth(local, 32 << 20, 50)
+        line["roofline"].update({"bound": "l2", "peak": l2, "frac": achieved / l2,
+                                 "peak_source": "measured live: cmg_l2_read_bandwidth (32 MiB x 50 reads, CUDA "
+                                                "events)", "hbm_peak": peak, "hbm_frac": achieved / peak})
+        pipes = ROOT / "profiles" / "pipes.json"
+        if pipes.exists():
+            key = f"config{args.config}_{args.dtype}_{args.precision}_l1"
+            pd = json.loads(pipes.read_text()).get(key)
+            if pd:
+                line["roofline"]["compute"] = pd
     if args.config == 3 and args.dtype == "float64" and args.precision == "exact":
-        line["roofline"]["note"] = ("1024^2 fp64 exact: u and f (16 MiB) stay in the 126 MB L2 and the level-1 "
-                                    "kernel is FP64-pipe bound (8 correctly rounded sqrt + div per pixel, ncu "
-                                    "profiles/r01/ncu); the HBM roofline binds at 16384^2: roofline_fine_level")
+        line["roofline"]["note"] = ("1024^2 fp64 exact: u and f (16 MiB) stay in the 126 MB L2; the level-1 "
+                                    "kernel is FP64-pipe / latency bound (8 correctly rounded sqrt + 10 div per "
+                                    "pixel: roofline.compute from ncu), far below the L2 bandwidth; the HBM "
+                                    "roofline binds at 16384^2: roofline_fine_level")
     if rank == 0 and ws == 1 and not args.no_fine and args.config != 5:
         line["roofline_fine_level"] = fine_level_roofline(local, peak)
     if rank == 0 and ws == 1 and args.config == 3 and not args.no_fine:
-        line["config"]["other_precisions"] = other_precisions(local, args.steps)
+        line["detail"]["other_precisions"] = other_precisions(local, args.steps)
+    if rank == 0 and ws == 1 and args.config in (1, 2, 3):
+        line["e2e_dropin"] = dropin_e2e(args, c, eps, max_outer, px_sweeps)
+    if rank == 0 and ws == 1 and args.config == 3 and not args.no_cpu:
+        nb = numpy_reference_leg()
+        if nb:
+            line["cpu_baseline_numpy"] = nb
     if cpu:
         line["cpu_baseline"] = cpu
     if rank == 0:
@@ -413,6 +446,71 @@ def run_ours(args):
         plan.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def dropin_e2e(args, c, eps, max_outer, px_sweeps) -> dict:
+    """The drop-in call itself, end to end: paper_2204_07921_b200.denoise(Image,
+    SolverConfig) on a pageable numpy image (validation, H2D, solve, D2H,
+    trace objects), as a reference user calls curvemg.denoise."""
+    import paper_2204_07921_b200 as cmg
+    from paper_2204_07921_b200 import synth
+
+    f, _ = synth.config_input(args.config, 0, fp32=(args.dtype == "float32"))
+    cfg = cmg.SolverConfig(alpha=0.06, mode=c["mode"], layers=c["layers"], epsilon=eps, max_outer=max_outer,
+                           dtype=args.dtype, precision=args.precision)
+    img = cmg.Image(f, 1.0)
+    for _ in range(2):
+        cmg.denoise(img, cfg)
+    ts = []
+    for _ in range(max(args.steps, 3)):
+        t0 = time.perf_counter()
+        cmg.denoise(img, cfg)
+        ts.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(ts))
+    return {"value": px_sweeps / (ms * 1e-3) / 1e6, "unit": "Mpixel-sweeps/s", "ms_per_step": ms,
+            "path": "paper_2204_07921_b200.denoise(Image, SolverConfig), pageable numpy in/out"}
+
+
+def numpy_reference_leg() -> dict | None:
+    """The reference's own NumPy solver (curvemg.denoise, installed offline into
+    the git-ignored baseline/_ref) on config 3, threads=1 and threads=None, on
+    this host: BASELINE.md section 3's CPU reference numbers, recorded beside the
+    oracle-port baseline.  None when baseline/_ref is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "curvemg").exists():
+        return None
+    sys.path.insert(0, str(ref))
+    try:
+        import curvemg
+    except Exception:
+        return None
+    finally:
+        sys.path.pop(0)
+    from paper_2204_07921_b200 import synth
+
+    f, cl = synth.config_input(3, 0)
+    out = {"unit": "Mpixel-sweeps/s", "workload": "config 3 (1024^2 MC, eps 1e-6, J=3), one solve per leg",
+           "numpy": np.__version__, "cpu_model": _cpu_model(), "host_cores": os.cpu_count()}
+    for thr in (1, None):
+        cfg = curvemg.SolverConfig(alpha=0.06, mode="mean", layers=3, epsilon=1e-6, threads=thr)
+        t0 = time.perf_counter()
+        _, tr = curvemg.denoise(curvemg.Image(f, 1.0), cfg)
+        dt = time.perf_counter() - t0
+        key = "threads_1" if thr == 1 else "threads_none"
+        out[key] = {"seconds_per_solve": dt, "cycles": tr.iterations,
+                    "value": tr.iterations * 3 * f.size / dt / 1e6,
+                    "threads": cfg.resolved_threads()}
+    return out
+
+
+def _cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def l1_kernel_name(dtype: str, prec: str, m: int, n: int) -> str:

@@ -155,6 +155,15 @@ int cmg_plan_ssim(cmg_plan* plan, int a_index, int b_index, const double* window
 void* cmg_host_alloc(unsigned long long bytes);
 int cmg_host_free(void* p);
 
+/*
+ * Measurement helper (no reference counterpart): L2 read bandwidth of the
+ * device, the roofline denominator of L2-resident workloads (1024^2 fp64:
+ * u and f = 16 MiB).  Streams a `bytes`-sized buffer (<< 126 MB L2, e.g.
+ * 32 MiB) `reps` times with 16-byte loads from every SM (grid = SMs x 8 CTAs)
+ * after one warm-up pass; *gbs = bytes * reps / elapsed (CUDA events).
+ */
+int cmg_l2_read_bandwidth(int device, long long bytes, int reps, double* gbs);
+
 #ifdef __cplusplus
 }
 #endif

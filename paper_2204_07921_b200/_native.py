@@ -24,7 +24,7 @@ SYMBOLS = (
     "cmg_version", "cmg_last_error", "cmg_device_count", "cmg_plan_create", "cmg_plan_destroy", "cmg_solve",
     "cmg_solve_device", "cmg_sweep_layer", "cmg_energy", "cmg_plane_table", "cmg_plan_stats", "cmg_time_sweep",
     "cmg_host_alloc", "cmg_host_free", "cmg_plan_buffer", "cmg_buffer_upload", "cmg_buffer_download",
-    "cmg_level_step", "cmg_energy_partials", "cmg_ssim_batch", "cmg_plan_ssim",
+    "cmg_level_step", "cmg_energy_partials", "cmg_ssim_batch", "cmg_plan_ssim", "cmg_l2_read_bandwidth",
 )
 
 
@@ -69,6 +69,8 @@ def _declare(L):
     L.cmg_time_sweep.argtypes = [_vp, _i, _i, _i, _dp]
     L.cmg_host_alloc.restype = _vp
     L.cmg_host_alloc.argtypes = [ctypes.c_ulonglong]
+    L.cmg_l2_read_bandwidth.restype = _i
+    L.cmg_l2_read_bandwidth.argtypes = [_i, ctypes.c_longlong, _i, _dp]
     L.cmg_host_free.restype = _i
     L.cmg_host_free.argtypes = [_vp]
     L.cmg_plan_buffer.restype = _i
@@ -171,3 +173,12 @@ class Plan:
         if rc != CMG_OK:
             raise RuntimeError(f"cmg_time_sweep failed ({rc}): {last_error()}")
         return ms.value
+
+
+def l2_read_bandwidth(device: int = 0, nbytes: int = 32 << 20, reps: int = 50) -> float:
+    """Measured L2 read bandwidth in GB/s (cmg_l2_read_bandwidth)."""
+    out = ctypes.c_double(0.0)
+    rc = lib().cmg_l2_read_bandwidth(device, nbytes, reps, ctypes.byref(out))
+    if rc != CMG_OK:
+        raise RuntimeError(last_error())
+    return out.value

@@ -83,6 +83,18 @@ __global__ void k_cond(cudaGraphConditionalHandle h, const int* ndone, int B, in
     cudaGraphSetConditional(h, (*ndone < B) ? 1u : 0u);
 }
 
+// L2 bandwidth probe: every thread streams 16-byte words, `reps` passes
+__global__ void k_l2_read(const uint4* __restrict__ buf, long long n16, int reps, unsigned* sink) {
+    unsigned acc = 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (int r = 0; r < reps; ++r)
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
+            const uint4 v = __ldcg(buf + i);
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    if (acc == 0x9e3779b9u) sink[(blockIdx.x * blockDim.x + threadIdx.x) & 1048575] = acc;
+}
+
 std::vector<int> layer_sequence(int layers, int full) {
     std::vector<int> s;
     for (int j = 1; j <= layers; ++j) s.push_back(j);
@@ -1043,6 +1055,44 @@ int cmg_energy_partials(cmg_plan* P, int u_index, int prev_index, int use_ref, i
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, P->raw5, sizeof(double) * NSUM * P->B, cudaMemcpyDeviceToHost, P->stream));
     CK(cudaStreamSynchronize(P->stream));
+    return CMG_OK;
+}
+
+int cmg_l2_read_bandwidth(int device, long long bytes, int reps, double* gbs) {
+    if (!gbs || bytes < (1 << 20) || reps < 1) return fail(CMG_EINVAL, "bad arguments");
+    CK(cudaSetDevice(device));
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    const long long n16 = bytes / 16;
+    uint4* buf = nullptr;
+    unsigned* sink = nullptr;
+    CK(cudaMalloc(&buf, n16 * 16));
+    if (cudaMalloc(&sink, sizeof(unsigned) * 1024 * 1024) != cudaSuccess) {
+        cudaFree(buf);
+        return fail(CMG_ECUDA, "cudaMalloc");
+    }
+    cudaStream_t st;
+    cudaEvent_t e0, e1;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaMemsetAsync(buf, 1, n16 * 16, st);
+    const int grid = nsm * 8;
+    k_l2_read<<<grid, 256, 0, st>>>(buf, n16, 1, sink);  // warm: the buffer is L2-resident afterwards
+    cudaEventRecord(e0, st);
+    k_l2_read<<<grid, 256, 0, st>>>(buf, n16, reps, sink);
+    cudaEventRecord(e1, st);
+    cudaError_t e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+    cudaFree(buf);
+    cudaFree(sink);
+    if (e != cudaSuccess) return fail(CMG_ECUDA, cudaGetErrorString(e));
+    *gbs = (double)n16 * 16.0 * reps / (ms * 1e-3) / 1e9;
     return CMG_OK;
 }
 
