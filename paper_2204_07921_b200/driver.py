@@ -290,7 +290,7 @@ def denoise(f: Image, config, reference: Image | None = None) -> tuple[Image, Co
         raise SolverDivergence(f"objective became non-finite at outer iteration {traces[0].iterations + 1}")
     if st == N.CMG_ENONFINITE:
         raise ValueError("corrections must be finite")
-    return Image(u[0].astype(np.float64), f.peak), traces[0]
+    return Image._from_solver(u[0], f.peak), traces[0]
 
 
 def denoise_batch(fs, config, references=None, peak: float | None = None):
@@ -318,4 +318,4 @@ def denoise_batch(fs, config, references=None, peak: float | None = None):
             raise SolverDivergence(f"image {b}: objective became non-finite")
         if st == N.CMG_ENONFINITE:
             raise ValueError(f"image {b}: corrections must be finite")
-    return [(Image(u[b].astype(np.float64), pk), traces[b]) for b in range(stack.shape[0])]
+    return [(Image._from_solver(u[b], pk), traces[b]) for b in range(stack.shape[0])]

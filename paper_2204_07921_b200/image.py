@@ -49,6 +49,18 @@ class Image:
             arr.flags.writeable = False
         object.__setattr__(self, "data", arr)
 
+    @classmethod
+    def _from_solver(cls, arr: np.ndarray, peak: float) -> "Image":
+        """Wrap a freshly allocated solver output without re-validating or
+        copying it (the solver raises on non-finite corrections, so the
+        values are finite; the array is owned by the new Image)."""
+        arr = np.ascontiguousarray(arr, dtype=np.float64)
+        arr.flags.writeable = False
+        obj = object.__new__(cls)
+        object.__setattr__(obj, "data", arr)
+        object.__setattr__(obj, "peak", float(peak))
+        return obj
+
     @property
     def height(self) -> int:
         return self.data.shape[0]

@@ -97,7 +97,7 @@ def test_plane_table_generated_header_matches_python():
 
 def _header_symbols():
     txt = (ROOT / "include" / "cmg.h").read_text()
-    return sorted(set(re.findall(r"\b(cmg_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(cmg_[a-z0-9_]+)\s*\(", txt)))
 
 
 def test_header_and_binding_agree():
