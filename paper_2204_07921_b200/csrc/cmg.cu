@@ -261,16 +261,7 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
     CK(cudaMemsetAsync(P->ndone, 0, sizeof(int) * 2, P->stream));
     int cycles = 0, bodies = 0, init_launches = 0;
-    if (P->persist) {
-        CK(cudaEventRecord(P->e0, P->stream));
-        P->enq = 0;
-        cudaError_t e = (P->dtype == CMG_F64) ? persist_launch<double>(P, has_ref, full)
-                                              : persist_launch<float>(P, has_ref, full);
-        if (e != cudaSuccess) return fail(CMG_ECUDA, std::string("persistent launch: ") + cudaGetErrorString(e));
-        CK(cudaEventRecord(P->e1, P->stream));
-        CK(cudaStreamSynchronize(P->stream));
-        P->launches = P->enq;
-    } else {
+    {
         if (!P->no_graph) {
             rc = build_graph(P, full, has_ref);
             if (rc) return rc;
@@ -338,7 +329,7 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
             cycles = std::max(cycles, hs[b].cycle + ((hs[b].status == ST_DIVERGED || hs[b].status == ST_NONFINITE) ? 1 : 0));
     }
     P->cycles_run = cycles;
-    if (!P->persist) {
+    {
         // kernels executed on the device: set-up kernels + every kernel node of
         // every WHILE-body replay (a body holds 2 cycles on the fused path)
         const int per = P->fused ? 2 : 1;
@@ -523,16 +514,10 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
             }
         }
     }
-    if (const char* lt = getenv("CMG_L1_TILE")) P->l1_tile = atoi(lt) != 0;
     // packed level-1 kernel: 56 x 120 tiles for large images (less halo per pixel,
     // 16384^2: 1.03 vs 1.11 ms), 56 x 56 otherwise (more CTAs for small images)
     if ((long long)m * n >= (4LL << 20) && n >= 240) P->l1x2 = 4;
     if (const char* lx = getenv("CMG_L1X2")) P->l1x2 = atoi(lx);
-    if (const char* v2 = getenv("CMG_FCFG2")) P->fcfg2 = atoi(v2);
-    if (const char* ct = getenv("CMG_COARSE_TILE")) P->coarse_tile = atoi(ct) != 0;
-    if (const char* cp = getenv("CMG_COOP")) P->coop = atoi(cp) != 0;
-    if (const char* co = getenv("CMG_COOP_OCC")) P->coop_occ = std::max(1, atoi(co));
-    if (const char* v3 = getenv("CMG_FCFG3")) P->fcfg3 = atoi(v3);
     auto bail = [&](int rc) {
         cmg_plan_destroy(P);
         return rc;
@@ -594,9 +579,7 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
         for (int j = 1; j <= std::min(layers, 3); ++j) fgen = fgen || P->lv[j].general;
         const char* fe = getenv("CMG_FUSED");
         P->fused = !fgen && !(fe && fe[0] == '0');
-        const char* pe = getenv("CMG_PERSIST");
-        P->persist = !P->fused && !gen && batch <= 1024 && (pe && pe[0] == '1');
-        if (const char* oc = getenv("CMG_OCC")) P->occ_cap = std::max(1, atoi(oc));
+        (void)gen;
     }
     {
         const char* te = getenv("CMG_TMA");

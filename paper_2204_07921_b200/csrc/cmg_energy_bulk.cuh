@@ -172,25 +172,29 @@ __global__ void __launch_bounds__(288) k_energy_bulk(EnergyArgs a, EnergyFin fz,
 #pragma unroll
                             for (int j = 0; j < PX; ++j) rv[j] = T(0);
                         }
-                        A tv[NSUM][PX];
+                        // per-pixel terms accumulate in fp64 (fp32 images: the curvature
+                        // term is evaluated in fp32, the fidelity / rel_u / PSNR terms from
+                        // exact fp64 differences of the fp32 values)
+                        double tv[NSUM][PX];
 #pragma unroll
                         for (int j = 0; j < PX; ++j) {
                             const A cc = C[j + 1];
-                            tv[0][j] = curv_term<A>(cc, C[j + 2], C[j], N[j + 1], S[j + 1], N[j + 2], S[j], N[j],
-                                                    S[j + 2], a.mode);
-                            const A d = cc - fv[j];
+                            tv[0][j] = (double)curv_term<A>(cc, C[j + 2], C[j], N[j + 1], S[j + 1], N[j + 2], S[j],
+                                                            N[j], S[j + 2], a.mode);
+                            const double c64 = (double)cc;
+                            const double d = c64 - (double)fv[j];
                             tv[1][j] = d * d;
-                            tv[2][j] = fabs(cc - pv[j]);
-                            tv[3][j] = fabs(cc);
-                            const A dr = cc - rv[j];
+                            tv[2][j] = fabs(c64 - (double)pv[j]);
+                            tv[3][j] = fabs(c64);
+                            const double dr = c64 - (double)rv[j];
                             tv[4][j] = dr * dr;
                         }
 #pragma unroll
                         for (int s = 0; s < NSUM; ++s) {
-                            A v = tv[s][0];
+                            double v = tv[s][0];
                             if (PX == 2) v = tv[s][0] + tv[s][1];
                             if (PX == 4) v = (tv[s][0] + tv[s][1]) + (tv[s][2] + tv[s][3]);
-                            acc[s] += (double)v;
+                            acc[s] += v;
                         }
                     }
 #pragma unroll

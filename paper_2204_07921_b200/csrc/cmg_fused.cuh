@@ -64,150 +64,4 @@ struct FusedArgs {
     int fs_ld;
 };
 
-template <int LAYER, int TP>
-struct FusedGeom {
-    static constexpr int S = (1 << LAYER) - 1;
-    static constexpr int HALO = 3;
-    static constexpr int RD = (TP + 2 * HALO) * S + 2;  // region side in pixels
-};
-
-template <typename T, int LAYER, int MODE, int PREC, int TP, int TS, class Acc>
-__device__ __forceinline__ void fused_phases(const Acc& U, const Acc& F, T* su, int ld, int r0, int c0,
-                                             const FusedArgs<T>& a, int P0, int Q0, int b) {
-    constexpr int S = (1 << LAYER) - 1;
-    SweepArgs<T> s;
-    s.u = nullptr;
-    s.f = nullptr;
-    s.m = a.m;
-    s.n = a.n;
-    s.layer = LAYER;
-    s.s = S;
-    s.r = 1 << (LAYER - 1);
-    s.P = a.P;
-    s.st = a.st;
-    s.dbg = 0;
-    s.bk.inner = a.P->inner;
-    s.bk.w0 = a.P->w[LAYER][0];
-    s.bk.den0 = a.P->den[LAYER][0];
-    s.bk.inv0 = 1.0 / s.bk.den0;
-    const int tid = threadIdx.x;
-    bool bad = false;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-        const int p = c >> 1, q = c & 1;
-        const int h = 3 - c;
-        // patch rows a in [P0-h, P0+TP+h) with a = p (mod 2), clipped to the grid
-        int alo = max(P0 - h, 0), ahi = min(P0 + TP + h, a.mj);
-        int blo = max(Q0 - h, 0), bhi = min(Q0 + TP + h, a.nj);
-        alo += ((alo & 1) != p);
-        blo += ((blo & 1) != q);
-        const int na = ahi > alo ? (ahi - alo + 1) / 2 : 0;
-        const int nb = bhi > blo ? (bhi - blo + 1) / 2 : 0;
-        const int cnt = na * nb;
-        s.p = p;
-        s.q = q;
-        s.hc = a.hc[c];
-        s.wc = a.wc[c];
-        s.flat = (s.wc == 1);
-        s.single = (s.hc * s.wc == 1);
-        if constexpr (TS == 1) {
-            for (int t = tid; t < cnt; t += blockDim.x) {
-                const int ai = alo + 2 * (t / nb), bi = blo + 2 * (t % nb);
-                const int R0 = ai * S, C0 = bi * S;
-                const T cv = patch_solve_ct<T, LAYER, MODE, PREC>(U, F, R0, C0, s);
-                bad |= !isfinite(cv);
-                const int r1 = min(R0 + S, a.m), c1 = min(C0 + S, a.n);
-                for (int i = R0; i < r1; ++i)
-                    for (int k = C0; k < c1; ++k) {
-                        T* pp = su + (i - r0) * ld + (k - c0);
-                        *pp = X<T>::add(*pp, cv);
-                    }
-            }
-        } else {
-            const int nteams = blockDim.x / TS;
-            const int team = tid / TS, lane = tid % TS;
-            for (int base = 0; base < cnt; base += nteams) {  // uniform trip count
-                int t = base + team;
-                const bool valid = t < cnt;
-                if (!valid) t = cnt - 1;
-                const int ai = alo + 2 * (t / nb), bi = blo + 2 * (t % nb);
-                const int R0 = ai * S, C0 = bi * S;
-                const T cv = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, s);
-                if (valid) {
-                    if (lane == 0) bad |= !isfinite(cv);
-                    for (int e = lane; e < S * S; e += TS) {
-                        const int i = R0 + e / S, k = C0 + e % S;
-                        if (i < a.m && k < a.n) {
-                            T* pp = su + (i - r0) * ld + (k - c0);
-                            *pp = X<T>::add(*pp, cv);
-                        }
-                    }
-                }
-            }
-        }
-        __syncthreads();
-    }
-    if (__syncthreads_or(bad) && tid == 0) a.st[b].bad = 1;
-}
-
-template <typename T, int LAYER, int MODE, int PREC, int TP, int TS>
-__device__ __noinline__ void fused_phases_border(T* su, T* sf, int ld, int r0, int c0, const FusedArgs<T>& a, int P0,
-                                                 int Q0, int b) {
-    SmemRefl<T> U{su, ld, r0, c0, a.m, a.n}, F{sf, ld, r0, c0, a.m, a.n};
-    fused_phases<T, LAYER, MODE, PREC, TP, TS>(U, F, su, ld, r0, c0, a, P0, Q0, b);
-}
-
-template <typename T, int LAYER, int MODE, int PREC, int TP, int TS>
-__global__ void __launch_bounds__(256) k_level_fused(FusedArgs<T> a) {
-    pdl_sync();  // blockDim <= 256
-    using G = FusedGeom<LAYER, TP>;
-    constexpr int S = G::S, RD = G::RD;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* su = reinterpret_cast<T*>(smem_raw);
-    T* sf = su + RD * RD;
-    const int b = blockIdx.z;
-    const int tr = blockIdx.x / a.tiles_c, tc = blockIdx.x % a.tiles_c;
-    const int P0 = tr * TP, Q0 = tc * TP;
-    const int r0 = (P0 - 3) * S - 1, c0 = (Q0 - 3) * S - 1;
-    const T* uin = a.uin + (long long)b * a.istride;
-    const T* f = a.f + (long long)b * a.istride;
-    T* uout = a.uout + (long long)b * a.istride;
-    if (a.st[b].done) {  // stopped image: carry u along the buffer rotation
-        const int ti0 = P0 * S, ti1 = min((P0 + TP) * S, a.m);
-        const int tk0 = Q0 * S, tk1 = min((Q0 + TP) * S, a.n);
-        const int tw = tk1 - tk0;
-        for (int e = threadIdx.x; e < (ti1 - ti0) * tw; e += blockDim.x) {
-            const long long g = (long long)(ti0 + e / tw) * a.n + (tk0 + e % tw);
-            uout[g] = uin[g];
-        }
-        return;
-    }
-    // stage the in-image part of the region
-    const int ilo = max(r0, 0), ihi = min(r0 + RD, a.m);
-    const int klo = max(c0, 0), khi = min(c0 + RD, a.n);
-    const int w = khi - klo;
-    for (int e = threadIdx.x; e < (ihi - ilo) * w; e += blockDim.x) {
-        const int i = ilo + e / w, k = klo + e % w;
-        const long long g = (long long)i * a.n + k;
-        su[(i - r0) * RD + (k - c0)] = uin[g];
-        sf[(i - r0) * RD + (k - c0)] = f[g];
-    }
-    __syncthreads();
-    const bool inside = (r0 >= 0) && (c0 >= 0) && (r0 + RD <= a.m) && (c0 + RD <= a.n);
-    if (inside) {
-        SmemDirect<T> U{su, RD, r0, c0}, F{sf, RD, r0, c0};
-        fused_phases<T, LAYER, MODE, PREC, TP, TS>(U, F, su, RD, r0, c0, a, P0, Q0, b);
-    } else {
-        fused_phases_border<T, LAYER, MODE, PREC, TP, TS>(su, sf, RD, r0, c0, a, P0, Q0, b);
-    }
-    // write the tile's own pixels
-    const int ti0 = P0 * S, ti1 = min((P0 + TP) * S, a.m);
-    const int tk0 = Q0 * S, tk1 = min((Q0 + TP) * S, a.n);
-    const int tw = tk1 - tk0;
-    for (int e = threadIdx.x; e < (ti1 - ti0) * tw; e += blockDim.x) {
-        const int i = ti0 + e / tw, k = tk0 + e % tw;
-        uout[(long long)i * a.n + k] = su[(i - r0) * RD + (k - c0)];
-    }
-}
-
 }  // namespace cmg

@@ -863,26 +863,28 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 1) k_energy(EnergyArgs a, 
             A nw, nc, ne, cw, cc, ce, sw, sc, se;
             ldrow(i0 - 1, nw, nc, ne);
             ldrow(i0, cw, cc, ce);
-            A loc[NSUM] = {0, 0, 0, 0, 0};
+            // per-pixel terms accumulate in fp64 (fp32 images: the curvature term is
+            // evaluated in fp32, the other terms from exact fp64 differences)
+            double loc[NSUM] = {0, 0, 0, 0, 0};
             int cnt = 0;
             for (int i = i0; i < i1; ++i) {
                 ldrow(i + 1, sw, sc, se);
                 const long long e = (long long)i * n + k;
-                const A fv = (A)f[e], pv = (A)up[e];
-                loc[0] += curv_term<A>(cc, ce, cw, nc, sc, ne, sw, nw, se, a.mode);
-                const A d = cc - fv;
+                const double fv = (double)f[e], pv = (double)up[e], c64 = (double)cc;
+                loc[0] += (double)curv_term<A>(cc, ce, cw, nc, sc, ne, sw, nw, se, a.mode);
+                const double d = c64 - fv;
                 loc[1] += d * d;
-                loc[2] += fabs(cc - pv);
-                loc[3] += fabs(cc);
+                loc[2] += fabs(c64 - pv);
+                loc[3] += fabs(c64);
                 if (rf) {
-                    const A dr = cc - (A)rf[e];
+                    const double dr = c64 - (double)rf[e];
                     loc[4] += dr * dr;
                 }
-                if (++cnt == 8) {  // fp32 images: short partial sums, then fp64
+                if (++cnt == 8) {  // 8-row partial sums, then the band accumulators
 #pragma unroll
                     for (int s = 0; s < NSUM; ++s) {
-                        acc[s] += (double)loc[s];
-                        loc[s] = A(0);
+                        acc[s] += loc[s];
+                        loc[s] = 0.0;
                     }
                     cnt = 0;
                 }
@@ -890,7 +892,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 1) k_energy(EnergyArgs a, 
                 cw = sw; cc = sc; ce = se;
             }
 #pragma unroll
-            for (int s = 0; s < NSUM; ++s) acc[s] += (double)loc[s];
+            for (int s = 0; s < NSUM; ++s) acc[s] += loc[s];
         }
     }
     energy_reduce_finalize(acc, a, fz, b);

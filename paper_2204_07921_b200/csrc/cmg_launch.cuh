@@ -12,7 +12,6 @@
 #include "cmg_l1x2.cuh"
 #include "cmg_coarse.cuh"
 #include "cmg_energy_bulk.cuh"
-#include "cmg_persist.cuh"
 #include "cmg_rowpair.cuh"
 #include "cmg_plan.h"
 
@@ -249,61 +248,6 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
 template <typename T>
 void enqueue_energy(cmg_plan* P, bool has_ref, double* eonly, int initial) {
     enqueue_energy_ptrs<T>(P, P->u, P->uprev, has_ref, eonly, initial, nullptr, 0, -1);
-}
-
-// tile sizes (patches per tile side), lanes per patch and CTA size of the
-// fused levels; variant v selected per plan (CMG_FCFG2 / CMG_FCFG3)
-template <int LAYER, int V>
-struct FusedCfg;
-template <>
-struct FusedCfg<1, 0> {
-    static constexpr int TP = 32, TS = 1, NT = 256;
-};
-template <>
-struct FusedCfg<2, 0> {
-    static constexpr int TP = 8, TS = 4, NT = 256;
-};
-template <>
-struct FusedCfg<2, 1> {
-    static constexpr int TP = 16, TS = 1, NT = 128;
-};
-template <>
-struct FusedCfg<2, 2> {
-    static constexpr int TP = 16, TS = 4, NT = 256;
-};
-template <>
-struct FusedCfg<2, 3> {
-    static constexpr int TP = 32, TS = 1, NT = 256;
-};
-template <>
-struct FusedCfg<3, 0> {
-    static constexpr int TP = 4, TS = 8, NT = 256;
-};
-template <>
-struct FusedCfg<3, 1> {
-    static constexpr int TP = 8, TS = 1, NT = 128;
-};
-template <>
-struct FusedCfg<3, 2> {
-    static constexpr int TP = 8, TS = 8, NT = 256;
-};
-template <>
-struct FusedCfg<3, 3> {
-    static constexpr int TP = 4, TS = 1, NT = 64;
-};
-
-template <typename T, int LAYER, int MODE, int PREC, int V>
-void launch_fused(cmg_plan* P, const FusedArgs<T>& a) {
-    constexpr int TP = FusedCfg<LAYER, V>::TP, TS = FusedCfg<LAYER, V>::TS, NT = FusedCfg<LAYER, V>::NT;
-    constexpr int RD = FusedGeom<LAYER, TP>::RD;
-    const size_t smem = 2 * sizeof(T) * RD * RD;
-    auto kern = k_level_fused<T, LAYER, MODE, PREC, TP, TS>;
-    smem_attr(kern, smem);
-    const Level& L = P->lv[LAYER];
-    FusedArgs<T> b = a;
-    const int tiles_r = (L.mj + TP - 1) / TP;
-    b.tiles_c = (L.nj + TP - 1) / TP;
-    klaunch(P, kern, dim3(tiles_r * b.tiles_c, 1, P->B), NT, smem, b);
 }
 
 template <typename T>
@@ -548,35 +492,12 @@ void dispatch_fused(cmg_plan* P, int layer, const FusedArgs<T>& a) {
         dispatch_rowpair<T, MODE, PREC>(P, layer, a);
         return;
     }
-    if (layer >= 2 && P->coarse_tile) {
-        if (layer == 2)
-            launch_coarse<T, 2, MODE, PREC>(P, a);
-        else
-            launch_coarse<T, 3, MODE, PREC>(P, a);
-        return;
-    }
-    if (layer == 1) {
-        if (P->l1_tile)
-            launch_l1_tile<T, MODE, PREC>(P, a);
-        else
-            launch_fused<T, 1, MODE, PREC, 0>(P, a);
-    } else if (layer == 2) {
-        switch (P->fcfg2) {
-            case 2: launch_fused<T, 2, MODE, PREC, 2>(P, a); break;
-            default: launch_fused<T, 2, MODE, PREC, 0>(P, a); break;
-        }
-    } else {
-        switch (P->fcfg3) {
-            case 2:
-                if (sizeof(T) == 4) {
-                    launch_fused<T, 3, MODE, PREC, 2>(P, a);
-                    break;
-                }
-                launch_fused<T, 3, MODE, PREC, 0>(P, a);
-                break;
-            default: launch_fused<T, 3, MODE, PREC, 0>(P, a); break;
-        }
-    }
+    if (layer == 1)
+        launch_l1_tile<T, MODE, PREC>(P, a);
+    else if (layer == 2)
+        launch_coarse<T, 2, MODE, PREC>(P, a);
+    else
+        launch_coarse<T, 3, MODE, PREC>(P, a);
 }
 
 template <typename T>
@@ -632,18 +553,7 @@ void enqueue_body_fused(cmg_plan* P, int full, bool has_ref) {
         const int target = (half == 0) ? 1 : 0;
         int other = 3 - prev - target;
         bool first = true;
-        std::vector<int> pending;  // consecutive non-fused coarse levels -> one cooperative kernel
-        auto flush = [&]() {
-            if (pending.empty()) return;
-            enqueue_coop<T>(P, P->ubuf[cur], pending.data(), (int)pending.size());
-            pending.clear();
-        };
         for (int j : seq) {
-            if (P->coop && !fusedj(j) && j >= 2 && !P->lv[j].general) {
-                pending.push_back(j);
-                continue;
-            }
-            flush();
             if (fusedj(j)) {
                 int out;
                 if (first) {
@@ -661,7 +571,6 @@ void enqueue_body_fused(cmg_plan* P, int full, bool has_ref) {
                 P->u = save;
             }
         }
-        flush();
         enqueue_energy_ptrs<T>(P, P->ubuf[cur], P->ubuf[prev], has_ref, nullptr, 0, nullptr, 0, -1);
     }
 }
@@ -672,140 +581,6 @@ void enqueue_fpads(cmg_plan* P) {
         Level& L = P->lv[j];
         if (L.general) enqueue_pad<T>(P, P->f, L.fpad, L.H, L.W, L.pstride, 1 + L.mp - P->m, 1 + L.np - P->n, false);
     }
-}
-
-template <typename T, int MODE, int PREC>
-cudaError_t persist_launch_v(cmg_plan* P, bool has_ref, int full) {
-    auto kern = k_persist<T, MODE, PREC, 4, 16>;
-    PersistArgs a;
-    memset(&a, 0, sizeof(a));
-    a.u = P->u;
-    a.uprev = P->uprev;
-    a.f = P->f;
-    a.ref = has_ref ? P->ref : nullptr;
-    a.has_ref = has_ref ? 1 : 0;
-    a.N = P->N;
-    a.m = P->m;
-    a.n = P->n;
-    a.B = P->B;
-    a.nseq = 0;
-    for (int j = 1; j <= P->layers; ++j) a.seq[a.nseq++] = j;
-    if (full)
-        for (int j = P->layers - 1; j >= 1; --j) a.seq[a.nseq++] = j;
-    for (int j = 1; j <= P->layers; ++j) {
-        const Level& L = P->lv[j];
-        a.side[j] = L.s;
-        for (int c = 0; c < 4; ++c) {
-            const int p = c >> 1, q = c & 1;
-            a.hc[j][c] = (L.mj - p + 1) / 2;
-            a.wc[j][c] = (L.nj - q + 1) / 2;
-        }
-    }
-    a.P = P->P;
-    a.st = P->st;
-    a.tr.energy = P->tr[0];
-    a.tr.rel_e = P->tr[1];
-    a.tr.rel_u = P->tr[2];
-    a.tr.psnr = P->tr[3];
-    a.tr.seconds = P->tr[4];
-    a.tr.cap = P->cap;
-    a.tr.ndone = P->ndone;
-    a.tr.eonly = nullptr;
-    a.tr.raw5 = nullptr;
-    const size_t smem = sizeof(double) * P->B + sizeof(int) * ((P->B + 1) & ~1) + sizeof(double) * NSUM * 32 +
-                        sizeof(T) * (64 + 256 + 2);
-    cudaError_t e;
-    if (P->pgrid == 0) {
-        int nb = 0, dev = 0, nsm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 256, smem);
-        if (e != cudaSuccess) return e;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (nb < 1) return cudaErrorCooperativeLaunchTooLarge;
-        P->pgrid = nsm * std::min(nb, P->occ_cap);
-    }
-    a.npieces = std::max(1, P->pgrid / P->B);
-    a.piece = (P->N + a.npieces - 1) / a.npieces;
-    a.npieces = (int)((P->N + a.piece - 1) / a.piece);
-    const int need = a.npieces * P->B;
-    if (need > P->pcap) {
-        if (P->partials) cudaFree(P->partials);
-        e = cudaMalloc(&P->partials, sizeof(double) * NSUM * (size_t)need);
-        if (e != cudaSuccess) return e;
-        P->pcap = need;
-    }
-    a.partials = P->partials;
-    void* args[] = {&a};
-    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(P->pgrid), dim3(256), args, smem, P->stream);
-    P->enq += 1;
-    return e;
-}
-
-// cooperative launch of levels seq[0..nseq) (all >= 2) in place on buffer u
-template <typename T, int MODE, int PREC>
-void coop_launch_v(cmg_plan* P, void* u, const int* seq, int nseq) {
-    auto kern = k_coarse_coop<T, MODE, PREC, 4, 16>;
-    PersistArgs a;
-    memset(&a, 0, sizeof(a));
-    a.u = u;
-    a.f = P->f;
-    a.N = P->N;
-    a.m = P->m;
-    a.n = P->n;
-    a.B = P->B;
-    a.nseq = nseq;
-    for (int i = 0; i < nseq; ++i) a.seq[i] = seq[i];
-    for (int j = 1; j <= P->layers; ++j) {
-        const Level& L = P->lv[j];
-        a.side[j] = L.s;
-        for (int c = 0; c < 4; ++c) {
-            a.hc[j][c] = (L.mj - (c >> 1) + 1) / 2;
-            a.wc[j][c] = (L.nj - (c & 1) + 1) / 2;
-        }
-    }
-    a.P = P->P;
-    a.st = P->st;
-    const size_t smem = 16 * ((P->B * sizeof(int) + 15) / 16) + sizeof(T) * (64 + 256 + 2);
-    // grid sized per plan and device: occupancy depends on the batch-sized
-    // dynamic shared memory and on the device the plan lives on
-    int grid = 0;
-    {
-        int nb = 0, nsm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 256, smem);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P->device);
-        grid = nsm * std::max(1, std::min(nb, P->coop_occ));
-    }
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = P->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-    if (e != cudaSuccess && P->launch_err == cudaSuccess) P->launch_err = e;
-    P->enq += 1;
-}
-
-template <typename T>
-void enqueue_coop(cmg_plan* P, void* u, const int* seq, int nseq) {
-    if (P->mode == CMG_MODE_GAUSS)
-        coop_launch_v<T, MODE_GAUSS, PREC_EXACT>(P, u, seq, nseq);
-    else if (P->prec == CMG_PREC_FAST)
-        coop_launch_v<T, MODE_MEAN, PREC_FAST>(P, u, seq, nseq);
-    else
-        coop_launch_v<T, MODE_MEAN, PREC_EXACT>(P, u, seq, nseq);
-}
-
-template <typename T>
-cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full) {
-    if (P->mode == CMG_MODE_GAUSS) return persist_launch_v<T, MODE_GAUSS, PREC_EXACT>(P, has_ref, full);
-    if (P->prec == CMG_PREC_FAST) return persist_launch_v<T, MODE_MEAN, PREC_FAST>(P, has_ref, full);
-    return persist_launch_v<T, MODE_MEAN, PREC_EXACT>(P, has_ref, full);
 }
 
 // k_energy_bulk geometry: band height H (halved until the items fill the
@@ -843,12 +618,10 @@ int energy_bulk_cfg_impl(int batch, int m, int n, int px, int ns, int* H_out) {
     template void cmg::enqueue_copy_prev<T>(cmg_plan*);                             \
     template void cmg::enqueue_fpads<T>(cmg_plan*);                             \
     template void cmg::enqueue_fsums<T>(cmg_plan*);                             \
-    template cudaError_t cmg::persist_launch<T>(cmg_plan*, bool, int);               \
     template void cmg::enqueue_fused_level<T>(cmg_plan*, int, const void*, void*);  \
     template void cmg::enqueue_energy_ptrs<T>(cmg_plan*, const void*, const void*, bool, double*, int, double*, \
                                               long long, long long);                                   \
     template void cmg::enqueue_body_fused<T>(cmg_plan*, int, bool);                  \
-    template void cmg::enqueue_coop<T>(cmg_plan*, void*, const int*, int);           \
     template <>                                                                     \
     int cmg::coarse_region<T>(int layer) {                                          \
         return cmg::coarse_region_impl<T>(layer);                                   \

@@ -60,15 +60,9 @@ struct cmg_plan {
     unsigned long long cur_cond = 0;  // conditional handle while capturing the WHILE body
     unsigned long long* stamps = nullptr;  // CMG_STAMPS diagnostics buffer
     int stamps_cap = 0;
-    bool l1_tile = true;
     int l1x2 = 1;  // packed fp32x2 level-1 kernel (fp32 fast mean); variants in launch_l1_tile
-    int fcfg2 = 0, fcfg3 = 0;
-    bool coarse_tile = true;  // k_coarse_tile for fused levels 2-3
-    bool coop = false;        // cooperative kernel for runs of non-fused coarse levels
-    int coop_occ = 4;         // max CTAs per SM of that kernel
-    cudaError_t launch_err = cudaSuccess;  // first failed checked launch (cooperative path)
     bool tma_ok[4] = {false, false, false, false};
-    CUtensorMap tmap[4][4];  // [level][buffer 0..2 = u rotation, 3 = f]  // fused L2/L3 tile variants (FusedCfg)  // dedicated level-1 tile kernel (k_l1_tile) instead of k_level_fused<1>  // diagnostics bits (CMG_DBG), see SweepArgs::dbg  // team sizes (lanes per patch) of levels 2 and 3
+    CUtensorMap tmap[4][4];  // [level][buffer 0..2 = u rotation, 3 = f]
     // graphs
     cudaGraphExec_t exec = nullptr;
     int gkey = -1;
@@ -85,11 +79,8 @@ struct cmg_plan {
     bool fused = false;
     int fuse_mask = 7;  // bit j-1: level j runs as one fused tile kernel (bit 0 required)
     void* ubuf[3] = {nullptr, nullptr, nullptr};  // rotation buffers (ubuf[0]=u, ubuf[1]=uprev)
-    // persistent cooperative path
-    bool persist = false;
-    int pgrid = 0;          // CTAs of the persistent kernel
-    int pcap = 0;           // partials capacity (images*pieces)
-    int occ_cap = 4;        // max CTAs per SM for the persistent kernel
+    int pcap = 0;           // partials capacity (images x energy CTAs)
+    cudaError_t launch_err = cudaSuccess;  // first failed checked launch
     int rowpair = 3;        // bit j-2: level j (2, 3) runs as two row-parity launches (k_rowpair)
     bool l1_wide = false;   // k_l1_tile with 32 x 64 tiles (CMG_L1_WIDE)
     int rp_ts2 = 4;         // lanes per patch of the level-2 row-parity kernel (CMG_RP_TS2)
@@ -167,8 +158,6 @@ void enqueue_fpads(cmg_plan* P);
 template <typename T>
 void enqueue_fsums(cmg_plan* P);
 template <typename T>
-cudaError_t persist_launch(cmg_plan* P, bool has_ref, int full);
-template <typename T>
 void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout);
 template <typename T>
 void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has_ref, double* eonly, int initial,
@@ -180,6 +169,5 @@ int coarse_region(int layer);
 template <typename T>
 int energy_bulk_cfg(int batch, int m, int n, int px, int ns, int* H);
 template <typename T>
-void enqueue_coop(cmg_plan* P, void* u, const int* seq, int nseq);
 bool make_tmap(CUtensorMap* out, const void* base, int esz, int m, int n, int B, int box);
 }  // namespace cmg

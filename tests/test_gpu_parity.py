@@ -202,3 +202,22 @@ def test_virtual_strips_equal_single_gpu_solve(parts, mode, dtype):
     assert t1.iterations == t2.iterations
     rtol = 1e-12 if dtype == "float64" else 1e-9
     assert np.allclose(t1.energies(), t2.energies(), rtol=rtol, atol=0)
+
+
+def test_nonfinite_energy_raises_solver_divergence():
+    """f ~ U[0,1) * 1e306: the level-1 curvature sum overflows, the
+    corrections stay finite (their plane normals overflow to inf, so the
+    distances are 0), and the energy after cycle 1 is inf -> the reference
+    raises SolverDivergence("objective became non-finite at outer iteration 1")
+    (driver.py:300-303; checked against curvemg in the build container)."""
+    rng = np.random.default_rng(0)
+    f = rng.random((32, 32)) * 1e306
+    r = O.denoise(f, max_outer=3)
+    assert r["status"] == 3 and r["iterations"] == 1
+    with pytest.raises(cmg.SolverDivergence, match="outer iteration 1"):
+        cmg.denoise(cmg.Image(f, 1.0), cmg.SolverConfig(max_outer=3))
+    out = None
+    with pytest.raises(cmg.SolverDivergence):
+        out = cmg.denoise_batch([cmg.Image(f, 1.0), cmg.Image(np.full((32, 32), 0.5), 1.0)],
+                                cmg.SolverConfig(max_outer=3))
+    assert out is None

@@ -23,10 +23,7 @@ ROOT = Path(__file__).resolve().parents[1]
 VARIANTS = {
     "fused_all_tma": {"CMG_FUSE_MASK": "7"},
     "fused_all_no_tma": {"CMG_FUSE_MASK": "7", "CMG_TMA": "0"},
-    "fused_generic_tiles": {"CMG_FUSE_MASK": "7", "CMG_COARSE_TILE": "0", "CMG_L1_TILE": "0"},
-    "cooperative_coarse": {"CMG_FUSE_MASK": "1", "CMG_COOP": "1"},
     "per_colour_only": {"CMG_FUSED": "0"},
-    "persistent_kernel": {"CMG_FUSED": "0", "CMG_PERSIST": "1"},
     "host_chunked_graph": {"CMG_NO_WHILE": "1"},
     "plain_stream_launches": {"CMG_NO_GRAPH": "1"},
     "separate_finalize": {"CMG_FUSED_FINALIZE": "0"},
@@ -126,6 +123,11 @@ VARIANTS32_CLOSE = {
     "fused_all": {"CMG_FUSE_MASK": "7"},
     "per_colour_only": {"CMG_FUSED": "0"},
     "per_colour_f_pixels": {"CMG_FUSED": "0", "CMG_FSUM": "0"},
+    # the large-job row-parity kernels (one thread per patch) forced on this small image
+    "row_parity_bulk_1_stage": {"CMG_ROWPAIR": "3", "CMG_RP1": "3"},
+    "row_parity_bulk_2_stages_128": {"CMG_ROWPAIR": "3", "CMG_RP1": "3", "CMG_RP_STAGES": "2", "CMG_RP_NT": "128"},
+    "row_parity_bulk_32_threads": {"CMG_ROWPAIR": "3", "CMG_RP1": "3", "CMG_RP_NT": "32"},
+    "row_parity_one_thread_ldg": {"CMG_ROWPAIR": "3", "CMG_RP1": "3", "CMG_RP_BULK": "0"},
 }
 
 

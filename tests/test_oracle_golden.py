@@ -97,3 +97,14 @@ def test_numpy_pairwise_restatement():
     for n in (1, 7, 8, 9, 127, 128, 129, 1000, 4096 + 3, 65536):
         a = rng.standard_normal(n) * np.exp(rng.standard_normal(n) * 4)
         assert O.lib().orc_pairwise_sum(a.ctypes.data_as(O._dp), n) == a.sum()
+
+
+def test_oracle_divergence_status():
+    """The reference raises SolverDivergence at outer iteration 1 for
+    f = U[0,1) * 1e306 (seed 0, 32x32; driver.py:300-303, run here against
+    curvemg); the oracle reports status 3 after one cycle."""
+    rng = np.random.default_rng(0)
+    f = rng.random((32, 32)) * 1e306
+    r = O.denoise(f, max_outer=3)
+    assert r["status"] == 3 and r["iterations"] == 1
+    assert not np.isfinite(r["energies"][1])
