@@ -15,11 +15,13 @@ from .driver import (
     TraceRecord,
     denoise,
     denoise_batch,
+    energy,
     rel_err_energy,
     rel_err_u,
 )
 from .image import Image, NoiseSpec, add_gaussian_noise, psnr
 from .metrics import ssim, ssim_batch
+from .phantoms import phantom
 from .planes import planes as plane_table
 
 __all__ = [
@@ -30,6 +32,7 @@ __all__ = [
     "TraceRecord",
     "denoise",
     "denoise_batch",
+    "energy",
     "rel_err_energy",
     "rel_err_u",
     "Image",
@@ -39,6 +42,7 @@ __all__ = [
     "ssim",
     "ssim_batch",
     "plane_table",
+    "phantom",
 ]
 
 __version__ = "0.1.0"
