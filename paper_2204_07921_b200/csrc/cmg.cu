@@ -112,6 +112,13 @@ void enqueue_cycle_T(cmg_plan* P, int full, bool has_ref) {
 }
 
 void enqueue_cycle(cmg_plan* P, int full, bool has_ref) {
+    if (P->efuse) {
+        if (P->dtype == CMG_F64)
+            enqueue_body_efused<double>(P, full, has_ref);
+        else
+            enqueue_body_efused<float>(P, full, has_ref);
+        return;
+    }
     if (P->fused) {
         if (P->dtype == CMG_F64)
             enqueue_body_fused<double>(P, full, has_ref);
@@ -271,14 +278,18 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
         const size_t bytes = P->esz * (size_t)P->N * P->B;
         CK(cudaMemcpyAsync(P->u, P->f, bytes, cudaMemcpyDeviceToDevice, P->stream));
         if (!P->fused) CK(cudaMemcpyAsync(P->uprev, P->f, bytes, cudaMemcpyDeviceToDevice, P->stream));
+        // initial energy (cycle 0): a separate pass, or the first level-1 kernel of the
+        // energy-fused body
         if (P->dtype == CMG_F64) {
             enqueue_fpads<double>(P);
             enqueue_fsums<double>(P);
-            enqueue_energy_ptrs<double>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1, nullptr, 0, -1);
+            if (!P->efuse)
+                enqueue_energy_ptrs<double>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1, nullptr, 0, -1);
         } else {
             enqueue_fpads<float>(P);
             enqueue_fsums<float>(P);
-            enqueue_energy_ptrs<float>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1, nullptr, 0, -1);
+            if (!P->efuse)
+                enqueue_energy_ptrs<float>(P, P->u, P->fused ? P->u : P->uprev, has_ref, nullptr, 1, nullptr, 0, -1);
         }
         CK(cudaGetLastError());
         if (P->launch_err != cudaSuccess) {
@@ -294,8 +305,10 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
             bodies = -1;  // counted from the per-image cycle counters below
         } else {
             int chunk = 1, launched = 0;
-            const int per = P->fused ? 2 : 1;
-            const int maxb = (max_outer + per - 1) / per;
+            // cycles per body; the energy-fused body needs one more level-1 visit (the
+            // energy of the last cycle is computed by the next cycle's level-1 kernel)
+            const int per = P->efuse ? efused_cycles_per_body(P, full) : (P->fused ? 2 : 1);
+            const int maxb = (max_outer + (P->efuse ? 1 : 0) + per - 1) / per;
             while (true) {
                 const int c = std::min(chunk, maxb - launched);
                 for (int i = 0; i < c; ++i) {
@@ -332,8 +345,8 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
     {
         // kernels executed on the device: set-up kernels + every kernel node of
         // every WHILE-body replay (a body holds 2 cycles on the fused path)
-        const int per = P->fused ? 2 : 1;
-        if (bodies < 0) bodies = std::max(1, (cycles + per - 1) / per);
+        const int per = P->efuse ? efused_cycles_per_body(P, full) : (P->fused ? 2 : 1);
+        if (bodies < 0) bodies = std::max(1, (cycles + (P->efuse ? 1 : 0) + per - 1) / per);
         P->launches = (long long)init_launches + (long long)bodies * P->nodes_per_cycle;
     }
     if (P->stamps) {
@@ -631,8 +644,19 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     if (getenv("CMG_VERBOSE"))
         fprintf(stderr, "cmg plan %dx%dx%d: energy CTAs/image %d (bulk px %d ns %d H %d), fused L2 %d L3 %d\n", m,
                 n, batch, P->nbx, P->eb_px, P->eb_ns, P->eb_H, (P->fuse_mask >> 1) & 1, (P->fuse_mask >> 2) & 1);
-    CKP(cudaMalloc(&P->partials, sizeof(double) * NSUM * (size_t)P->nbx * batch));
-    P->pcap = P->nbx * batch;
+    if (const char* ff = getenv("CMG_FUSED_FINALIZE")) P->fused_finalize = atoi(ff) != 0;
+    // energy-fused cycles: the level-1 tile kernel (k_l1_tile; fp32 fast mean keeps the
+    // packed k_l1_x2 kernel and the separate bulk energy pass) sums the energy of its
+    // input; partials per level-1 CTA (tiles >= 32 x 32)
+    {
+        const bool x2 = dtype == CMG_F32 && P->prec == CMG_PREC_FAST && mode == CMG_MODE_MEAN && P->l1x2;
+        P->efuse = P->fused && P->fused_finalize && !x2;
+        if (const char* ef = getenv("CMG_EFUSE")) P->efuse = P->efuse && atoi(ef) != 0;
+    }
+    const long long l1tiles = (long long)((m + 31) / 32) * ((n + 31) / 32);
+    const long long nparts = std::max<long long>(P->nbx, P->efuse ? l1tiles : 0);
+    CKP(cudaMalloc(&P->partials, sizeof(double) * NSUM * (size_t)nparts * batch));
+    P->pcap = (int)(nparts * batch);
     CKP(cudaMalloc(&P->st, sizeof(ImgState) * batch));
     CKP(cudaMalloc(&P->ndone, sizeof(int) * 2));
     P->iters = P->ndone + 1;
@@ -640,7 +664,6 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     CKP(cudaMalloc(&P->raw5, sizeof(double) * NSUM * batch));
     CKP(cudaMalloc(&P->tickets, sizeof(int) * (batch + 1)));
     CKP(cudaMemset(P->tickets, 0, sizeof(int) * (batch + 1)));
-    if (const char* ff = getenv("CMG_FUSED_FINALIZE")) P->fused_finalize = atoi(ff) != 0;
     if (const char* pd = getenv("CMG_PDL")) P->pdl = atoi(pd) != 0;
     // 32 x 64 level-1 tiles once they fill the GPU (1024^2 fp64 exact: 48.7 -> 47.3 us,
     // 4096^2: 643 -> 579 us; 512^2 has too few: 20.3 -> 27.2 us)

@@ -371,8 +371,9 @@ __global__ void __launch_bounds__(NT) k_coarse_tile(FusedArgs<T> a, const __grid
     const int ti0 = P0 * S, ti1 = min((P0 + TP) * S, m);
     const int tk0 = Q0 * S, tk1 = min((Q0 + TP) * S, n);
     if (a.st[b].done) {
+        const T* xd = a.xdone + (long long)b * a.istride;
         for (int i = ti0 + threadIdx.x / 32; i < ti1; i += NT / 32)
-            for (int k = tk0 + (threadIdx.x & 31); k < tk1; k += 32) uout[(long long)i * n + k] = uin[(long long)i * n + k];
+            for (int k = tk0 + (threadIdx.x & 31); k < tk1; k += 32) uout[(long long)i * n + k] = xd[(long long)i * n + k];
         return;
     }
     if constexpr (TS > 1) {

@@ -55,6 +55,13 @@ struct ImgState {
     int status;       // ST_*
     int bad;          // non-finite correction seen during the current cycle
     unsigned long long t0;
+    // energy-fused cycle (the level-1 kernel of cycle g+1 computes and finalizes
+    // the energy of u_g): started = the initial record exists; bad1 = non-finite
+    // correction in the level-1 sweep now running, bad1_prev = in the previous
+    // cycle's level-1 sweep (its later levels report through `bad`)
+    int started;
+    int bad1;
+    int bad1_prev;
 };
 
 template <typename T>
@@ -659,12 +666,16 @@ struct TraceArgs {
 // Finalize one image (one CTA): reduce its partials in a fixed order, record
 // the trace and apply the stopping rule (driver.py:294-310).  Returns true
 // if the image is (now) done.
-__device__ __forceinline__ void finalize_image(int b, const double* partials, int nbx, const SolveParams* P,
-                                               ImgState* st, const TraceArgs& tr, int initial) {
+// initial: 1 = record cycle 0, 0 = record the next cycle, 2 = energy-fused
+// cycle (record 0 if the image has not started, else the next cycle; the
+// non-finite flag of the cycle is `bad` | `bad1_prev`).  `shf` is >= NSUM x 256
+// doubles of shared scratch; the first 256 threads reduce (block size >= 256).
+__device__ __forceinline__ void finalize_image_s(int b, const double* partials, int nbx, const SolveParams* P,
+                                                 ImgState* st, const TraceArgs& tr, int initial, double (*shf)[256]) {
     ImgState& S = st[b];
+    const bool efused = initial == 2;
+    if (efused) initial = S.started ? 0 : 1;
     if (!initial && tr.eonly == nullptr && tr.raw5 == nullptr && S.done) return;
-    // the first 256 threads reduce (any block size >= 256 may call this)
-    __shared__ double shf[NSUM][256];
     const int tid = threadIdx.x;
     double acc[NSUM] = {0, 0, 0, 0, 0};
     if (tid < 256) {
@@ -706,6 +717,11 @@ __device__ __forceinline__ void finalize_image(int b, const double* partials, in
         S.done = 0;
         S.status = ST_RUNNING;
         S.bad = 0;
+        S.started = 1;
+        if (efused) {
+            S.bad1_prev = S.bad1;
+            S.bad1 = 0;
+        }
         S.t0 = now;
         tr.energy[base] = F;
         tr.rel_e[base] = __longlong_as_double(0x7ff8000000000000ULL);
@@ -715,7 +731,14 @@ __device__ __forceinline__ void finalize_image(int b, const double* partials, in
         return;
     }
     const int kk = S.cycle + 1;
-    if (S.bad) {
+    int badc = S.bad;
+    if (efused) {
+        badc |= S.bad1_prev;
+        S.bad1_prev = S.bad1;
+        S.bad1 = 0;
+        S.bad = 0;
+    }
+    if (badc) {
         S.status = ST_NONFINITE;
         S.done = 1;
         atomicAdd(tr.ndone, 1);
@@ -748,6 +771,12 @@ __device__ __forceinline__ void finalize_image(int b, const double* partials, in
         S.done = 1;
         atomicAdd(tr.ndone, 1);
     }
+}
+
+__device__ __forceinline__ void finalize_image(int b, const double* partials, int nbx, const SolveParams* P,
+                                               ImgState* st, const TraceArgs& tr, int initial) {
+    __shared__ double shf[NSUM][256];
+    finalize_image_s(b, partials, nbx, P, st, tr, initial, shf);
 }
 
 static __global__ void __launch_bounds__(256) k_finalize(const double* partials, int nbx, const SolveParams* P,
@@ -807,6 +836,57 @@ __device__ __forceinline__ void energy_reduce_finalize(const double (&acc)[NSUM]
     __threadfence();
     if (tid == 0) fz.tickets[b] = 0;
     finalize_image(b, a.partials, a.nbx, fz.P, fz.stw, fz.tr, fz.initial);
+    if (fz.cond == 0ULL || tid != 0) return;
+    __threadfence();
+    if (atomicAdd(fz.img_ticket, 1) == fz.B - 1) {
+        *fz.img_ticket = 0;
+        __threadfence();
+        cudaGraphSetConditional((cudaGraphConditionalHandle)fz.cond, (*((volatile int*)fz.tr.ndone) < fz.B) ? 1u : 0u);
+    }
+}
+
+// ---- energy fused into a level-1 tile kernel (energy-fused cycle) ----------
+// (1) at the start, the CTA's fp64 sums of its owned pixels -> partials[b][cta]
+static __device__ __noinline__ void cta_sums_store(const double (&acc)[NSUM], double* partials, int nbx, int cta,
+                                            int b) {
+    __shared__ double sh[NSUM][32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int s = 0; s < NSUM; ++s) {
+        double v = acc[s];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) sh[s][wid] = v;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+#pragma unroll
+        for (int s = 0; s < NSUM; ++s) {
+            double v = lane < nw ? sh[s][lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) partials[((long long)b * nbx + cta) * NSUM + s] = v;
+        }
+    }
+}
+
+// (2) at the end (shared memory free), the ticket: the image's last CTA
+// finalizes it (fixed-order reduction of the partials, trace, stopping rule)
+// using `scratch` (>= NSUM x 256 doubles), and the last image sets the WHILE
+// condition.  Every CTA of every image calls this, stopped images included.
+static __device__ __noinline__ void efused_ticket(const EnergyFin& fz, const double* partials, int nbx, int b,
+                                           double* scratch) {
+    __shared__ int last;
+    const int tid = threadIdx.x;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = (atomicAdd(&fz.tickets[b], 1) == nbx - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (tid == 0) fz.tickets[b] = 0;
+    finalize_image_s(b, partials, nbx, fz.P, fz.stw, fz.tr, 2, reinterpret_cast<double (*)[256]>(scratch));
     if (fz.cond == 0ULL || tid != 0) return;
     __threadfence();
     if (atomicAdd(fz.img_ticket, 1) == fz.B - 1) {

@@ -199,8 +199,46 @@ __device__ __forceinline__ void l1_reflect_fix(T* su, int r0, int c0, int m, int
     __syncthreads();
 }
 
+// Energy terms of the tile's owned pixels from the staged (pristine) region:
+// level-1 curvature from the 3x3 neighbourhood (closed form, as k_energy),
+// fidelity from sf, |u - u_prev| and (u - ref)^2 from global memory; fp64
+// accumulation; CTA sums -> partials (tangent.energy, tangent.py:325-341;
+// driver.py:284-291, :161-166)
+template <typename T, int TH, int TW>
+__device__ __noinline__ void l1_energy_sums(const FusedArgs<T>& a, const T* su, const T* sf, int R, int C, int b,
+                                               int cta, int nbx) {
+    using G = L1Geom<T, TH, TW>;
+    const int m = a.m, n = a.n;
+    const T* up = a.uprev + (long long)b * a.istride;
+    const T* rf = a.ref ? a.ref + (long long)b * a.istride : nullptr;
+    double acc[NSUM] = {0, 0, 0, 0, 0};
+    for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
+        const int i = e / TW, k = e % TW;
+        const int gi = R + i, gk = C + k;
+        if (gi >= m || gk >= n) continue;
+        const int ri = i + G::HALO, rk = k + G::HALO;
+        const T c = su[G::idx(ri, rk)];
+        const T t = curv_term<T>(c, su[G::idx(ri, rk + 1)], su[G::idx(ri, rk - 1)], su[G::idx(ri - 1, rk)],
+                                 su[G::idx(ri + 1, rk)], su[G::idx(ri - 1, rk + 1)], su[G::idx(ri + 1, rk - 1)],
+                                 su[G::idx(ri - 1, rk - 1)], su[G::idx(ri + 1, rk + 1)], a.mode);
+        const long long g = (long long)gi * n + gk;
+        const double c64 = (double)c;
+        const double d = c64 - (double)sf[G::idx(ri, rk)];
+        acc[0] += (double)t;
+        acc[1] += d * d;
+        acc[2] += fabs(c64 - (double)up[g]);
+        acc[3] += fabs(c64);
+        if (rf) {
+            const double dr = c64 - (double)rf[g];
+            acc[4] += dr * dr;
+        }
+    }
+    cta_sums_store(acc, a.partials, nbx, cta, b);
+}
+
+// (mean mode: 4 CTAs of 256 threads per SM, <= 64 registers)
 template <typename T, int MODE, int PREC, int TH, int TW>
-__global__ void __launch_bounds__(256) k_l1_tile(FusedArgs<T> a) {
+__global__ void __launch_bounds__(256, MODE == MODE_MEAN ? 4 : 1) k_l1_tile(FusedArgs<T> a) {
     pdl_sync();
     using G = L1Geom<T, TH, TW>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -213,11 +251,14 @@ __global__ void __launch_bounds__(256) k_l1_tile(FusedArgs<T> a) {
     const T* f = a.f + (long long)b * a.istride;
     T* uout = a.uout + (long long)b * a.istride;
     const int m = a.m, n = a.n;
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x, nbx = gridDim.x * gridDim.y;
     if (a.st[b].done) {  // stopped image: carry u along the buffer rotation
+        const T* xd = a.xdone + (long long)b * a.istride;
         for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
             const int i = R + e / TW, k = C + e % TW;
-            if (i < m && k < n) uout[(long long)i * n + k] = uin[(long long)i * n + k];
+            if (i < m && k < n) uout[(long long)i * n + k] = xd[(long long)i * n + k];
         }
+        if (a.efuse) efused_ticket(a.fz, a.partials, nbx, b, reinterpret_cast<double*>(smem_raw));
         return;
     }
     const int r0 = R - G::HALO, c0 = C - G::HALO;
@@ -234,6 +275,7 @@ __global__ void __launch_bounds__(256) k_l1_tile(FusedArgs<T> a) {
     __syncthreads();
     const bool border = (r0 < 1) || (c0 < 1) || (r0 + G::RH >= m) || (c0 + G::RW >= n);
     if (border) l1_reflect_fix<T, TH, TW>(su, r0, c0, m, n);
+    if (a.efuse) l1_energy_sums<T, TH, TW>(a, su, sf, R, C, b, cta, nbx);
     bool bad = false;
     L1Back<T> bk;
     bk.P = a.P;
@@ -279,11 +321,20 @@ __global__ void __launch_bounds__(256) k_l1_tile(FusedArgs<T> a) {
         __syncthreads();
         if (border) l1_reflect_fix<T, TH, TW>(su, r0, c0, m, n);
     });
-    if (__syncthreads_or(bad) && threadIdx.x == 0) a.st[b].bad = 1;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) {
+        if (a.efuse)
+            a.st[b].bad1 = 1;
+        else
+            a.st[b].bad = 1;
+    }
     for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
         const int i = e / TW, k = e % TW;
         const int gi = R + i, gk = C + k;
         if (gi < m && gk < n) uout[(long long)gi * n + gk] = su[G::idx(i + G::HALO, k + G::HALO)];
+    }
+    if (a.efuse) {
+        __syncthreads();  // shared memory becomes the finalize scratch
+        efused_ticket(a.fz, a.partials, nbx, b, reinterpret_cast<double*>(smem_raw));
     }
 }
 

@@ -130,9 +130,10 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     float* uout = a.uout + (long long)b * a.istride;
     const int m = a.m, n = a.n;
     if (a.st[b].done) {
+        const float* xd = a.xdone + (long long)b * a.istride;
         for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
             const int i = R + e / TW, k = C + e % TW;
-            if (i < m && k < n) uout[(long long)i * n + k] = uin[(long long)i * n + k];
+            if (i < m && k < n) uout[(long long)i * n + k] = xd[(long long)i * n + k];
         }
         return;
     }

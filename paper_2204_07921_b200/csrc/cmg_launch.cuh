@@ -180,6 +180,33 @@ void enqueue_copy_prev(cmg_plan* P) {
     P->enq += 1;
 }
 
+inline TraceArgs make_trace_args(const cmg_plan* P, double* eonly, double* raw5) {
+    TraceArgs ta;
+    ta.energy = P->tr[0];
+    ta.rel_e = P->tr[1];
+    ta.rel_u = P->tr[2];
+    ta.psnr = P->tr[3];
+    ta.seconds = P->tr[4];
+    ta.cap = P->cap;
+    ta.ndone = P->ndone;
+    ta.eonly = eonly;
+    ta.raw5 = raw5;
+    return ta;
+}
+
+inline EnergyFin make_energy_fin(const cmg_plan* P, const TraceArgs& ta, int initial) {
+    EnergyFin fz;
+    fz.tr = ta;
+    fz.P = P->P;
+    fz.stw = P->st;
+    fz.tickets = P->fused_finalize ? P->tickets : nullptr;
+    fz.img_ticket = P->tickets + P->B;
+    fz.initial = initial;
+    fz.cond = P->cur_cond;
+    fz.B = P->B;
+    return fz;
+}
+
 template <typename T>
 void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has_ref, double* eonly, int initial,
                          double* raw5, long long e_lo, long long e_hi) {
@@ -202,25 +229,8 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
     ea.e_hi = e_hi < 0 ? P->N : e_hi;
     ea.partials = P->partials;
     ea.st = P->st;
-    TraceArgs ta;
-    ta.energy = P->tr[0];
-    ta.rel_e = P->tr[1];
-    ta.rel_u = P->tr[2];
-    ta.psnr = P->tr[3];
-    ta.seconds = P->tr[4];
-    ta.cap = P->cap;
-    ta.ndone = P->ndone;
-    ta.eonly = eonly;
-    ta.raw5 = raw5;
-    EnergyFin fz;
-    fz.tr = ta;
-    fz.P = P->P;
-    fz.stw = P->st;
-    fz.tickets = P->fused_finalize ? P->tickets : nullptr;
-    fz.img_ticket = P->tickets + P->B;
-    fz.initial = initial;
-    fz.cond = P->cur_cond;
-    fz.B = P->B;
+    const TraceArgs ta = make_trace_args(P, eonly, raw5);
+    EnergyFin fz = make_energy_fin(P, ta, initial);
     if (P->egeneral)
         klaunch(P, k_energy<T, SRC_PADDED>, dim3(P->nbx, P->B), 256, 0, ea, fz);
     else if (P->eb_px == 1)
@@ -373,12 +383,13 @@ inline int coarse_region_impl(int layer) {
 // levels 2-3: two launches (patch-row parity 0, then 1), each running its two
 // colours in a shared-memory window (cmg_rowpair.cuh); X -> Y
 template <typename T, int LAYER, int MODE, int PREC, int TS, int NT = 256>
-void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
+void launch_rowpair(cmg_plan* P, const T* X, T* Y, const T* Xd) {
     using G = RowPairGeom<LAYER, TS, NT>;
     const Level& L = P->lv[LAYER];
     RowPairArgs<T> r;
     r.X = X;
     r.Y = Y;
+    r.Xdone = Xd;
     r.nj = L.nj;
     r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
     // u window + f of the patch row (no f rows with per-patch f sums)
@@ -402,12 +413,13 @@ void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
 
 // persistent bulk-copy variant (one thread per patch, fast mean + f sums)
 template <typename T, int LAYER, int NT, int STAGES>
-void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y) {
+void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y, const T* Xd) {
     using G = RowPairGeom<LAYER, 1, NT, 16 / (int)sizeof(T)>;
     const Level& L = P->lv[LAYER];
     RowPairArgs<T> r;
     r.X = X;
     r.Y = Y;
+    r.Xdone = Xd;
     r.nj = L.nj;
     r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
     const size_t smem = STAGES * sizeof(T) * G::ROWS * G::WIN;
@@ -433,11 +445,11 @@ void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y) {
 }
 
 template <typename T, int LAYER, int NT>
-void launch_rowpair_bulk(cmg_plan* P, const T* X, T* Y) {
+void launch_rowpair_bulk(cmg_plan* P, const T* X, T* Y, const T* Xd) {
     if (P->rp_stages == 1)
-        launch_rowpair_bulk_s<T, LAYER, NT, 1>(P, X, Y);
+        launch_rowpair_bulk_s<T, LAYER, NT, 1>(P, X, Y, Xd);
     else
-        launch_rowpair_bulk_s<T, LAYER, NT, 2>(P, X, Y);
+        launch_rowpair_bulk_s<T, LAYER, NT, 2>(P, X, Y, Xd);
 }
 
 template <typename T, int MODE, int PREC>
@@ -450,39 +462,39 @@ void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
             if (P->rp_bulk && ((size_t)P->n * sizeof(T)) % 16 == 0) {
                 if (sizeof(T) == 4 && P->rp_nt == 128) {
                     if (layer == 2)
-                        launch_rowpair_bulk<T, 2, 128>(P, a.uin, a.uout);
+                        launch_rowpair_bulk<T, 2, 128>(P, a.uin, a.uout, a.xdone);
                     else
-                        launch_rowpair_bulk<T, 3, 128>(P, a.uin, a.uout);
+                        launch_rowpair_bulk<T, 3, 128>(P, a.uin, a.uout, a.xdone);
                 } else if (P->rp_nt == 32) {
                     if (layer == 2)
-                        launch_rowpair_bulk<T, 2, 32>(P, a.uin, a.uout);
+                        launch_rowpair_bulk<T, 2, 32>(P, a.uin, a.uout, a.xdone);
                     else
-                        launch_rowpair_bulk<T, 3, 32>(P, a.uin, a.uout);
+                        launch_rowpair_bulk<T, 3, 32>(P, a.uin, a.uout, a.xdone);
                 } else if (layer == 2) {
-                    launch_rowpair_bulk<T, 2, NT1>(P, a.uin, a.uout);
+                    launch_rowpair_bulk<T, 2, NT1>(P, a.uin, a.uout, a.xdone);
                 } else {
-                    launch_rowpair_bulk<T, 3, NT1>(P, a.uin, a.uout);
+                    launch_rowpair_bulk<T, 3, NT1>(P, a.uin, a.uout, a.xdone);
                 }
                 return;
             }
             if (layer == 2)
-                launch_rowpair<T, 2, MODE, PREC, 1, NT1>(P, a.uin, a.uout);
+                launch_rowpair<T, 2, MODE, PREC, 1, NT1>(P, a.uin, a.uout, a.xdone);
             else
-                launch_rowpair<T, 3, MODE, PREC, 1, NT1>(P, a.uin, a.uout);
+                launch_rowpair<T, 3, MODE, PREC, 1, NT1>(P, a.uin, a.uout, a.xdone);
             return;
         }
     }
     // team sizes: level 2 {4, 8} lanes per patch (P->rp_ts2), level 3 {8, 16}
     if (layer == 2) {
         if (P->rp_ts2 >= 8)
-            launch_rowpair<T, 2, MODE, PREC, 8>(P, a.uin, a.uout);
+            launch_rowpair<T, 2, MODE, PREC, 8>(P, a.uin, a.uout, a.xdone);
         else
-            launch_rowpair<T, 2, MODE, PREC, 4>(P, a.uin, a.uout);
+            launch_rowpair<T, 2, MODE, PREC, 4>(P, a.uin, a.uout, a.xdone);
     } else {
         if (P->ts3 >= 16)
-            launch_rowpair<T, 3, MODE, PREC, 16>(P, a.uin, a.uout);
+            launch_rowpair<T, 3, MODE, PREC, 16>(P, a.uin, a.uout, a.xdone);
         else
-            launch_rowpair<T, 3, MODE, PREC, 8>(P, a.uin, a.uout);
+            launch_rowpair<T, 3, MODE, PREC, 8>(P, a.uin, a.uout, a.xdone);
     }
 }
 
@@ -500,12 +512,26 @@ void dispatch_fused(cmg_plan* P, int layer, const FusedArgs<T>& a) {
         launch_coarse<T, 3, MODE, PREC>(P, a);
 }
 
+// one fused level visit uin -> uout; xdone: copy source of stopped images
+// (nullptr: uin); efuse_prev != nullptr: energy-fused level-1 visit whose
+// input is the cycle input u_g and efuse_prev is u_{g-1}
 template <typename T>
-void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
+void enqueue_fused_level_x(cmg_plan* P, int layer, const void* uin, void* uout, const void* xdone,
+                           const void* efuse_prev, bool has_ref) {
     const Level& L = P->lv[layer];
     FusedArgs<T> a;
+    memset(&a, 0, sizeof(a));
     a.uin = (const T*)uin;
     a.uout = (T*)uout;
+    a.xdone = (const T*)(xdone ? xdone : uin);
+    a.efuse = efuse_prev != nullptr;
+    if (a.efuse) {
+        a.uprev = (const T*)efuse_prev;
+        a.ref = has_ref ? (const T*)P->ref : nullptr;
+        a.partials = P->partials;
+        a.mode = P->mode;
+        a.fz = make_energy_fin(P, make_trace_args(P, nullptr, nullptr), 2);
+    }
     a.f = (const T*)P->f;
     a.istride = P->N;
     a.m = P->m;
@@ -533,6 +559,11 @@ void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
         dispatch_fused<T, MODE_MEAN, PREC_EXACT>(P, layer, a);
     P->enq += 1;
     stamp(P, 100 + layer);
+}
+
+template <typename T>
+void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
+    enqueue_fused_level_x<T>(P, layer, uin, uout, nullptr, nullptr, false);
 }
 
 // Two V-cycles per graph body with a 3-buffer rotation: fused levels write
@@ -572,6 +603,48 @@ void enqueue_body_fused(cmg_plan* P, int full, bool has_ref) {
             }
         }
         enqueue_energy_ptrs<T>(P, P->ubuf[cur], P->ubuf[prev], has_ref, nullptr, 0, nullptr, 0, -1);
+    }
+}
+
+// Energy-fused cycles.  The level-1 kernel of cycle g+1 also computes and
+// finalizes the energy of its input u_g (trace, stopping rule, WHILE
+// condition), so a cycle has no separate energy pass.  Buffer roles per cycle:
+// X = input u_g, Pv = u_{g-1} (read by that level-1 kernel for rel_u), Z = the
+// third buffer.  Level 1: X -> Z; the later fused levels alternate Z <-> Pv
+// (X stays intact: a stopped image's later levels copy u_g from it); in-place
+// levels run on the current buffer.  The next cycle's (X, Pv) = (output, X).
+// A graph body holds the 2 or 3 cycles after which the roles return to
+// (0, 1, 2).  Stopping: once cycle g is finalized as the last one, that image's
+// later levels copy u_g along, so after the body it is in buffer 0.
+template <typename T>
+void enqueue_body_efused(cmg_plan* P, int full, bool has_ref) {
+    std::vector<int> seq;
+    for (int j = 1; j <= P->layers; ++j) seq.push_back(j);
+    if (full)
+        for (int j = P->layers - 1; j >= 1; --j) seq.push_back(j);
+    auto fusedj = [&](int j) { return j <= 3 && ((P->fuse_mask >> (j - 1)) & 1); };
+    const int per = efused_cycles_per_body(P, full);
+    int X = 0, Pv = 1, Z = 2;
+    for (int h = 0; h < per; ++h) {
+        int cur = X;
+        bool first = true;
+        for (int j : seq) {
+            if (fusedj(j)) {
+                const int out = first ? Z : ((cur == Z) ? Pv : Z);
+                enqueue_fused_level_x<T>(P, j, P->ubuf[cur], P->ubuf[out], P->ubuf[X], first ? P->ubuf[Pv] : nullptr,
+                                         has_ref);
+                first = false;
+                cur = out;
+            } else {
+                void* save = P->u;
+                P->u = P->ubuf[cur];
+                for (int c = 0; c < 4; ++c) enqueue_sweep<T>(P, j, c);
+                P->u = save;
+            }
+        }
+        Pv = X;
+        X = cur;
+        Z = 3 - X - Pv;
     }
 }
 
@@ -622,6 +695,7 @@ int energy_bulk_cfg_impl(int batch, int m, int n, int px, int ns, int* H_out) {
     template void cmg::enqueue_energy_ptrs<T>(cmg_plan*, const void*, const void*, bool, double*, int, double*, \
                                               long long, long long);                                   \
     template void cmg::enqueue_body_fused<T>(cmg_plan*, int, bool);                  \
+    template void cmg::enqueue_body_efused<T>(cmg_plan*, int, bool);                 \
     template <>                                                                     \
     int cmg::coarse_region<T>(int layer) {                                          \
         return cmg::coarse_region_impl<T>(layer);                                   \

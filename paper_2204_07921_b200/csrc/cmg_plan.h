@@ -7,6 +7,7 @@
 #include <utility>
 #include <cuda_runtime.h>
 #include <mutex>
+#include <vector>
 #include <set>
 #include <utility>
 
@@ -80,6 +81,7 @@ struct cmg_plan {
     int fuse_mask = 7;  // bit j-1: level j runs as one fused tile kernel (bit 0 required)
     void* ubuf[3] = {nullptr, nullptr, nullptr};  // rotation buffers (ubuf[0]=u, ubuf[1]=uprev)
     int pcap = 0;           // partials capacity (images x energy CTAs)
+    bool efuse = false;     // energy-fused cycles (enqueue_body_efused; CMG_EFUSE=0: off)
     cudaError_t launch_err = cudaSuccess;  // first failed checked launch
     int rowpair = 3;        // bit j-2: level j (2, 3) runs as two row-parity launches (k_rowpair)
     bool l1_wide = false;   // k_l1_tile with 32 x 64 tiles (CMG_L1_WIDE)
@@ -164,6 +166,40 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
                          double* raw5, long long e_lo, long long e_hi);
 template <typename T>
 void enqueue_body_fused(cmg_plan* P, int full, bool has_ref);
+template <typename T>
+void enqueue_body_efused(cmg_plan* P, int full, bool has_ref);
+inline int efused_out(const cmg_plan* P, int full, int X, int Pv, int Z) {
+    int cur = X;
+    bool first = true;
+    std::vector<int> seq;
+    for (int j = 1; j <= P->layers; ++j) seq.push_back(j);
+    if (full)
+        for (int j = P->layers - 1; j >= 1; --j) seq.push_back(j);
+    for (int j : seq) {
+        if (!(j <= 3 && ((P->fuse_mask >> (j - 1)) & 1))) continue;
+        if (first) {
+            cur = Z;
+            first = false;
+        } else {
+            cur = (cur == Z) ? Pv : Z;
+        }
+    }
+    return cur;
+}
+
+inline int efused_cycles_per_body(const cmg_plan* P, int full) {
+    int X = 0, Pv = 1, Z = 2, k = 0;
+    do {
+        const int o = efused_out(P, full, X, Pv, Z);
+        Pv = X;
+        X = o;
+        Z = 3 - X - Pv;
+        ++k;
+    } while (!(X == 0 && Pv == 1) && k < 6);
+    return k;
+}
+
+
 template <typename T>
 int coarse_region(int layer);
 template <typename T>

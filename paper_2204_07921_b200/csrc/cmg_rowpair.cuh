@@ -33,6 +33,7 @@ template <typename T>
 struct RowPairArgs {
     const T* X;      // level input (u before this level)
     T* Y;            // level output
+    const T* Xdone;  // stopped images: copy source (the cycle input in the energy-fused cycle, else X)
     int ntiles;      // column tiles per patch row
     int nj;          // patch columns
     SweepArgs<T> c0, c1;  // colours (p,0) and (p,1): p, q, hc, wc, flat, single, backward constants
@@ -266,10 +267,11 @@ template <typename T, int LAYER, int TS, int NT>
 __device__ __forceinline__ void rp_copy_owned(const RowPairArgs<T>& a, const RPItem<T>& it) {
     using G = RowPairGeom<LAYER, TS, NT>;
     const int n = a.c0.n;
+    const T* xd = a.Xdone + (long long)it.b * a.c0.istride;
     for (int i = it.R0; i < it.orow1; ++i)
         for (int k = it.ok0 + threadIdx.x; k < it.ok1; k += G::NT) {
             const long long g = (long long)i * n + k;
-            it.Yb[g] = it.Xb[g];
+            it.Yb[g] = xd[g];
         }
 }
 
