@@ -300,6 +300,12 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
         init_launches = P->enq;
         if (P->use_while) {
             CK(cudaGraphLaunch(P->exec, P->stream));
+            if (P->fused) {  // stopped images whose final u is not in buffer 0
+                if (P->dtype == CMG_F64)
+                    enqueue_collect<double>(P);
+                else
+                    enqueue_collect<float>(P);
+            }
             CK(cudaEventRecord(P->e1, P->stream));
             CK(cudaStreamSynchronize(P->stream));
             bodies = -1;  // counted from the per-image cycle counters below
@@ -328,6 +334,12 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
                 if (nd >= P->B || launched >= maxb) break;
                 chunk = std::min(chunk * 2, 16);
             }
+            if (P->fused) {
+                if (P->dtype == CMG_F64)
+                    enqueue_collect<double>(P);
+                else
+                    enqueue_collect<float>(P);
+            }
             CK(cudaEventRecord(P->e1, P->stream));
             CK(cudaStreamSynchronize(P->stream));
             bodies = launched;
@@ -347,7 +359,7 @@ int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_oute
         // every WHILE-body replay (a body holds 2 cycles on the fused path)
         const int per = P->efuse ? efused_cycles_per_body(P, full) : (P->fused ? 2 : 1);
         if (bodies < 0) bodies = std::max(1, (cycles + (P->efuse ? 1 : 0) + per - 1) / per);
-        P->launches = (long long)init_launches + (long long)bodies * P->nodes_per_cycle;
+        P->launches = (long long)init_launches + (long long)bodies * P->nodes_per_cycle + (P->fused ? 1 : 0);
     }
     if (P->stamps) {
         std::vector<unsigned long long> sb(P->stamps_cap);

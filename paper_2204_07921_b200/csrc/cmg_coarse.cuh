@@ -370,12 +370,7 @@ __global__ void __launch_bounds__(NT) k_coarse_tile(FusedArgs<T> a, const __grid
     const int m = a.m, n = a.n;
     const int ti0 = P0 * S, ti1 = min((P0 + TP) * S, m);
     const int tk0 = Q0 * S, tk1 = min((Q0 + TP) * S, n);
-    if (a.st[b].done) {
-        const T* xd = a.xdone + (long long)b * a.istride;
-        for (int i = ti0 + threadIdx.x / 32; i < ti1; i += NT / 32)
-            for (int k = tk0 + (threadIdx.x & 31); k < tk1; k += 32) uout[(long long)i * n + k] = xd[(long long)i * n + k];
-        return;
-    }
+    if (a.st[b].done) return;  // stopped image (final u in ImgState::final_buf)
     if constexpr (TS > 1) {
         for (int l = threadIdx.x; l < G::NPL; l += NT) {
             const PlaneRT q = PlaneRT::getg(l);

@@ -62,9 +62,6 @@ struct FusedArgs {
     const double* fsum;  // fast mean: per-patch sums of f of this level (k_patch_fsum) or nullptr
     long long fs_img;
     int fs_ld;
-    // stopped images copy their pixels from xdone (the cycle's input buffer in the
-    // energy-fused cycle, else uin) to uout, carrying u along the buffer rotation
-    const T* xdone;
     // energy-fused level-1 visit (efuse = 1): the kernel also sums the energy terms of
     // its input (u_g: curvature, fidelity, |u - uprev|, |u|, (u - ref)^2) and its last
     // CTA per image finalizes cycle g (EnergyFin: trace, stopping rule, WHILE condition)

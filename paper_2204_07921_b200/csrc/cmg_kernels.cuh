@@ -62,6 +62,7 @@ struct ImgState {
     int started;
     int bad1;
     int bad1_prev;
+    int final_buf;  // rotation buffer holding the image's final u once it stopped (k_collect)
 };
 
 template <typename T>
@@ -670,8 +671,8 @@ struct TraceArgs {
 // cycle (record 0 if the image has not started, else the next cycle; the
 // non-finite flag of the cycle is `bad` | `bad1_prev`).  `shf` is >= NSUM x 256
 // doubles of shared scratch; the first 256 threads reduce (block size >= 256).
-__device__ __forceinline__ void finalize_image_s(int b, const double* partials, int nbx, const SolveParams* P,
-                                                 ImgState* st, const TraceArgs& tr, int initial, double (*shf)[256]) {
+static __device__ __noinline__ void finalize_image_s(int b, const double* partials, int nbx, const SolveParams* P,
+                                              ImgState* st, TraceArgs tr, int initial, double (*shf)[256], int buf) {
     ImgState& S = st[b];
     const bool efused = initial == 2;
     if (efused) initial = S.started ? 0 : 1;
@@ -740,6 +741,7 @@ __device__ __forceinline__ void finalize_image_s(int b, const double* partials, 
     }
     if (badc) {
         S.status = ST_NONFINITE;
+        S.final_buf = buf;
         S.done = 1;
         atomicAdd(tr.ndone, 1);
         return;
@@ -747,6 +749,7 @@ __device__ __forceinline__ void finalize_image_s(int b, const double* partials, 
     if (!isfinite(F)) {
         tr.energy[base + kk] = F;
         S.status = ST_DIVERGED;
+        S.final_buf = buf;
         S.done = 1;
         atomicAdd(tr.ndone, 1);
         return;
@@ -764,25 +767,27 @@ __device__ __forceinline__ void finalize_image_s(int b, const double* partials, 
     const double crit = (P->stop_rule == 0) ? re : ru;
     if (crit <= P->eps) {
         S.status = ST_CONVERGED;
+        S.final_buf = buf;
         S.done = 1;
         atomicAdd(tr.ndone, 1);
     } else if (kk >= P->max_outer) {
         S.status = ST_NOT_CONVERGED;
+        S.final_buf = buf;
         S.done = 1;
         atomicAdd(tr.ndone, 1);
     }
 }
 
 __device__ __forceinline__ void finalize_image(int b, const double* partials, int nbx, const SolveParams* P,
-                                               ImgState* st, const TraceArgs& tr, int initial) {
+                                               ImgState* st, const TraceArgs& tr, int initial, int buf = 0) {
     __shared__ double shf[NSUM][256];
-    finalize_image_s(b, partials, nbx, P, st, tr, initial, shf);
+    finalize_image_s(b, partials, nbx, P, st, tr, initial, shf, buf);
 }
 
 static __global__ void __launch_bounds__(256) k_finalize(const double* partials, int nbx, const SolveParams* P,
-                                                         ImgState* st, TraceArgs tr, int initial) {
+                                                         ImgState* st, TraceArgs tr, int initial, int buf) {
     pdl_sync();
-    finalize_image(blockIdx.x, partials, nbx, P, st, tr, initial);
+    finalize_image(blockIdx.x, partials, nbx, P, st, tr, initial, buf);
 }
 
 // Energy + finalize in one launch: 32x8 pixel tiles (grid-stride), per-CTA
@@ -799,6 +804,7 @@ struct EnergyFin {
     int initial;
     unsigned long long cond;  // cudaGraphConditionalHandle (0: none)
     int B;
+    int buf;  // rotation buffer index of the u being finalized (ImgState::final_buf)
 };
 
 // deterministic CTA reduction of the five sums -> partials[b][blockIdx.x];
@@ -835,7 +841,7 @@ __device__ __forceinline__ void energy_reduce_finalize(const double (&acc)[NSUM]
     if (!last) return;
     __threadfence();
     if (tid == 0) fz.tickets[b] = 0;
-    finalize_image(b, a.partials, a.nbx, fz.P, fz.stw, fz.tr, fz.initial);
+    finalize_image(b, a.partials, a.nbx, fz.P, fz.stw, fz.tr, fz.initial, fz.buf);
     if (fz.cond == 0ULL || tid != 0) return;
     __threadfence();
     if (atomicAdd(fz.img_ticket, 1) == fz.B - 1) {
@@ -847,8 +853,8 @@ __device__ __forceinline__ void energy_reduce_finalize(const double (&acc)[NSUM]
 
 // ---- energy fused into a level-1 tile kernel (energy-fused cycle) ----------
 // (1) at the start, the CTA's fp64 sums of its owned pixels -> partials[b][cta]
-static __device__ __noinline__ void cta_sums_store(const double (&acc)[NSUM], double* partials, int nbx, int cta,
-                                            int b) {
+__device__ __forceinline__ void cta_sums_store(const double (&acc)[NSUM], double* partials, int nbx, int cta,
+                                               int b) {
     __shared__ double sh[NSUM][32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 #pragma unroll
@@ -875,8 +881,8 @@ static __device__ __noinline__ void cta_sums_store(const double (&acc)[NSUM], do
 // finalizes it (fixed-order reduction of the partials, trace, stopping rule)
 // using `scratch` (>= NSUM x 256 doubles), and the last image sets the WHILE
 // condition.  Every CTA of every image calls this, stopped images included.
-static __device__ __noinline__ void efused_ticket(const EnergyFin& fz, const double* partials, int nbx, int b,
-                                           double* scratch) {
+__device__ __forceinline__ void efused_ticket(const EnergyFin& fz, const double* partials, int nbx, int b,
+                                              double* scratch) {
     __shared__ int last;
     const int tid = threadIdx.x;
     __threadfence();
@@ -886,7 +892,7 @@ static __device__ __noinline__ void efused_ticket(const EnergyFin& fz, const dou
     if (!last) return;
     __threadfence();
     if (tid == 0) fz.tickets[b] = 0;
-    finalize_image_s(b, partials, nbx, fz.P, fz.stw, fz.tr, 2, reinterpret_cast<double (*)[256]>(scratch));
+    finalize_image_s(b, partials, nbx, fz.P, fz.stw, fz.tr, 2, reinterpret_cast<double (*)[256]>(scratch), fz.buf);
     if (fz.cond == 0ULL || tid != 0) return;
     __threadfence();
     if (atomicAdd(fz.img_ticket, 1) == fz.B - 1) {
@@ -976,6 +982,19 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 1) k_energy(EnergyArgs a, 
         }
     }
     energy_reduce_finalize(acc, a, fz, b);
+}
+
+// After a solve: images whose final u is not in rotation buffer 0 (they
+// stopped in another cycle of the graph body; later kernels skipped them)
+template <typename T>
+__global__ void k_collect(T* u0, const T* u1, const T* u2, long long N, const ImgState* st) {
+    const int b = blockIdx.y;
+    const int fb = st[b].final_buf;
+    if (fb == 0) return;
+    const T* src = (fb == 1 ? u1 : u2) + (long long)b * N;
+    T* dst = u0 + (long long)b * N;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (long long)gridDim.x * blockDim.x)
+        dst[e] = src[e];
 }
 
 // Per-patch sums of the odd-padded f of one level (fast mean mode: f* =

@@ -205,12 +205,9 @@ __device__ __forceinline__ void l1_reflect_fix(T* su, int r0, int c0, int m, int
 // accumulation; CTA sums -> partials (tangent.energy, tangent.py:325-341;
 // driver.py:284-291, :161-166)
 template <typename T, int TH, int TW>
-__device__ __noinline__ void l1_energy_sums(const FusedArgs<T>& a, const T* su, const T* sf, int R, int C, int b,
-                                               int cta, int nbx) {
+__device__ __forceinline__ void l1_energy_sums(const T* su, const T* sf, int R, int C, int m, int n, const T* up,
+                                               const T* rf, int mode, double* partials, int b, int cta, int nbx) {
     using G = L1Geom<T, TH, TW>;
-    const int m = a.m, n = a.n;
-    const T* up = a.uprev + (long long)b * a.istride;
-    const T* rf = a.ref ? a.ref + (long long)b * a.istride : nullptr;
     double acc[NSUM] = {0, 0, 0, 0, 0};
     for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
         const int i = e / TW, k = e % TW;
@@ -220,7 +217,7 @@ __device__ __noinline__ void l1_energy_sums(const FusedArgs<T>& a, const T* su, 
         const T c = su[G::idx(ri, rk)];
         const T t = curv_term<T>(c, su[G::idx(ri, rk + 1)], su[G::idx(ri, rk - 1)], su[G::idx(ri - 1, rk)],
                                  su[G::idx(ri + 1, rk)], su[G::idx(ri - 1, rk + 1)], su[G::idx(ri + 1, rk - 1)],
-                                 su[G::idx(ri - 1, rk - 1)], su[G::idx(ri + 1, rk + 1)], a.mode);
+                                 su[G::idx(ri - 1, rk - 1)], su[G::idx(ri + 1, rk + 1)], mode);
         const long long g = (long long)gi * n + gk;
         const double c64 = (double)c;
         const double d = c64 - (double)sf[G::idx(ri, rk)];
@@ -233,7 +230,7 @@ __device__ __noinline__ void l1_energy_sums(const FusedArgs<T>& a, const T* su, 
             acc[4] += dr * dr;
         }
     }
-    cta_sums_store(acc, a.partials, nbx, cta, b);
+    cta_sums_store(acc, partials, nbx, cta, b);
 }
 
 // (mean mode: 4 CTAs of 256 threads per SM, <= 64 registers)
@@ -252,12 +249,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_MEAN ? 4 : 1) k_l1_tile(Fuse
     T* uout = a.uout + (long long)b * a.istride;
     const int m = a.m, n = a.n;
     const int cta = blockIdx.y * gridDim.x + blockIdx.x, nbx = gridDim.x * gridDim.y;
-    if (a.st[b].done) {  // stopped image: carry u along the buffer rotation
-        const T* xd = a.xdone + (long long)b * a.istride;
-        for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
-            const int i = R + e / TW, k = C + e % TW;
-            if (i < m && k < n) uout[(long long)i * n + k] = xd[(long long)i * n + k];
-        }
+    if (a.st[b].done) {  // stopped image (its final u stays in ImgState::final_buf)
         if (a.efuse) efused_ticket(a.fz, a.partials, nbx, b, reinterpret_cast<double*>(smem_raw));
         return;
     }
@@ -275,7 +267,10 @@ __global__ void __launch_bounds__(256, MODE == MODE_MEAN ? 4 : 1) k_l1_tile(Fuse
     __syncthreads();
     const bool border = (r0 < 1) || (c0 < 1) || (r0 + G::RH >= m) || (c0 + G::RW >= n);
     if (border) l1_reflect_fix<T, TH, TW>(su, r0, c0, m, n);
-    if (a.efuse) l1_energy_sums<T, TH, TW>(a, su, sf, R, C, b, cta, nbx);
+    if (a.efuse)
+        l1_energy_sums<T, TH, TW>(su, sf, R, C, m, n, a.uprev + (long long)b * a.istride,
+                                  a.ref ? a.ref + (long long)b * a.istride : nullptr, a.mode, a.partials, b, cta,
+                                  nbx);
     bool bad = false;
     L1Back<T> bk;
     bk.P = a.P;

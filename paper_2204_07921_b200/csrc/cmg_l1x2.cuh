@@ -129,14 +129,7 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     const float* f = a.f + (long long)b * a.istride;
     float* uout = a.uout + (long long)b * a.istride;
     const int m = a.m, n = a.n;
-    if (a.st[b].done) {
-        const float* xd = a.xdone + (long long)b * a.istride;
-        for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
-            const int i = R + e / TW, k = C + e % TW;
-            if (i < m && k < n) uout[(long long)i * n + k] = xd[(long long)i * n + k];
-        }
-        return;
-    }
+    if (a.st[b].done) return;  // stopped image (final u in ImgState::final_buf)
     const int r0 = R - G::HALO, c0 = C - G::HALO;
     const bool border = (r0 < 1) || (c0 < 1) || (r0 + G::RH >= m) || (c0 + G::RW >= n);
     const bool vec = !border && (n % 4 == 0);

@@ -180,6 +180,12 @@ void enqueue_copy_prev(cmg_plan* P) {
     P->enq += 1;
 }
 
+inline int buf_index(const cmg_plan* P, const void* u) {
+    for (int i = 0; i < 3; ++i)
+        if (u == P->ubuf[i]) return i;
+    return 0;
+}
+
 inline TraceArgs make_trace_args(const cmg_plan* P, double* eonly, double* raw5) {
     TraceArgs ta;
     ta.energy = P->tr[0];
@@ -194,7 +200,7 @@ inline TraceArgs make_trace_args(const cmg_plan* P, double* eonly, double* raw5)
     return ta;
 }
 
-inline EnergyFin make_energy_fin(const cmg_plan* P, const TraceArgs& ta, int initial) {
+inline EnergyFin make_energy_fin(const cmg_plan* P, const TraceArgs& ta, int initial, int buf) {
     EnergyFin fz;
     fz.tr = ta;
     fz.P = P->P;
@@ -204,6 +210,7 @@ inline EnergyFin make_energy_fin(const cmg_plan* P, const TraceArgs& ta, int ini
     fz.initial = initial;
     fz.cond = P->cur_cond;
     fz.B = P->B;
+    fz.buf = buf;
     return fz;
 }
 
@@ -230,7 +237,7 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
     ea.partials = P->partials;
     ea.st = P->st;
     const TraceArgs ta = make_trace_args(P, eonly, raw5);
-    EnergyFin fz = make_energy_fin(P, ta, initial);
+    EnergyFin fz = make_energy_fin(P, ta, initial, buf_index(P, u));
     if (P->egeneral)
         klaunch(P, k_energy<T, SRC_PADDED>, dim3(P->nbx, P->B), 256, 0, ea, fz);
     else if (P->eb_px == 1)
@@ -248,7 +255,7 @@ void enqueue_energy_ptrs(cmg_plan* P, const void* u, const void* uprev, bool has
         klaunch(P, k_energy<T, SRC_INPLACE>, dim3(P->nbx, P->B), 256, 0, ea, fz);
     stamp(P, 90);
     if (!P->fused_finalize) {
-        klaunch(P, k_finalize, P->B, 256, 0, P->partials, P->nbx, P->P, P->st, ta, initial);
+        klaunch(P, k_finalize, P->B, 256, 0, P->partials, P->nbx, P->P, P->st, ta, initial, buf_index(P, u));
         P->enq += 1;
         stamp(P, 91);
     }
@@ -383,13 +390,12 @@ inline int coarse_region_impl(int layer) {
 // levels 2-3: two launches (patch-row parity 0, then 1), each running its two
 // colours in a shared-memory window (cmg_rowpair.cuh); X -> Y
 template <typename T, int LAYER, int MODE, int PREC, int TS, int NT = 256>
-void launch_rowpair(cmg_plan* P, const T* X, T* Y, const T* Xd) {
+void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
     using G = RowPairGeom<LAYER, TS, NT>;
     const Level& L = P->lv[LAYER];
     RowPairArgs<T> r;
     r.X = X;
     r.Y = Y;
-    r.Xdone = Xd;
     r.nj = L.nj;
     r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
     // u window + f of the patch row (no f rows with per-patch f sums)
@@ -413,13 +419,12 @@ void launch_rowpair(cmg_plan* P, const T* X, T* Y, const T* Xd) {
 
 // persistent bulk-copy variant (one thread per patch, fast mean + f sums)
 template <typename T, int LAYER, int NT, int STAGES>
-void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y, const T* Xd) {
+void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y) {
     using G = RowPairGeom<LAYER, 1, NT, 16 / (int)sizeof(T)>;
     const Level& L = P->lv[LAYER];
     RowPairArgs<T> r;
     r.X = X;
     r.Y = Y;
-    r.Xdone = Xd;
     r.nj = L.nj;
     r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
     const size_t smem = STAGES * sizeof(T) * G::ROWS * G::WIN;
@@ -445,11 +450,11 @@ void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y, const T* Xd) {
 }
 
 template <typename T, int LAYER, int NT>
-void launch_rowpair_bulk(cmg_plan* P, const T* X, T* Y, const T* Xd) {
+void launch_rowpair_bulk(cmg_plan* P, const T* X, T* Y) {
     if (P->rp_stages == 1)
-        launch_rowpair_bulk_s<T, LAYER, NT, 1>(P, X, Y, Xd);
+        launch_rowpair_bulk_s<T, LAYER, NT, 1>(P, X, Y);
     else
-        launch_rowpair_bulk_s<T, LAYER, NT, 2>(P, X, Y, Xd);
+        launch_rowpair_bulk_s<T, LAYER, NT, 2>(P, X, Y);
 }
 
 template <typename T, int MODE, int PREC>
@@ -462,39 +467,39 @@ void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
             if (P->rp_bulk && ((size_t)P->n * sizeof(T)) % 16 == 0) {
                 if (sizeof(T) == 4 && P->rp_nt == 128) {
                     if (layer == 2)
-                        launch_rowpair_bulk<T, 2, 128>(P, a.uin, a.uout, a.xdone);
+                        launch_rowpair_bulk<T, 2, 128>(P, a.uin, a.uout);
                     else
-                        launch_rowpair_bulk<T, 3, 128>(P, a.uin, a.uout, a.xdone);
+                        launch_rowpair_bulk<T, 3, 128>(P, a.uin, a.uout);
                 } else if (P->rp_nt == 32) {
                     if (layer == 2)
-                        launch_rowpair_bulk<T, 2, 32>(P, a.uin, a.uout, a.xdone);
+                        launch_rowpair_bulk<T, 2, 32>(P, a.uin, a.uout);
                     else
-                        launch_rowpair_bulk<T, 3, 32>(P, a.uin, a.uout, a.xdone);
+                        launch_rowpair_bulk<T, 3, 32>(P, a.uin, a.uout);
                 } else if (layer == 2) {
-                    launch_rowpair_bulk<T, 2, NT1>(P, a.uin, a.uout, a.xdone);
+                    launch_rowpair_bulk<T, 2, NT1>(P, a.uin, a.uout);
                 } else {
-                    launch_rowpair_bulk<T, 3, NT1>(P, a.uin, a.uout, a.xdone);
+                    launch_rowpair_bulk<T, 3, NT1>(P, a.uin, a.uout);
                 }
                 return;
             }
             if (layer == 2)
-                launch_rowpair<T, 2, MODE, PREC, 1, NT1>(P, a.uin, a.uout, a.xdone);
+                launch_rowpair<T, 2, MODE, PREC, 1, NT1>(P, a.uin, a.uout);
             else
-                launch_rowpair<T, 3, MODE, PREC, 1, NT1>(P, a.uin, a.uout, a.xdone);
+                launch_rowpair<T, 3, MODE, PREC, 1, NT1>(P, a.uin, a.uout);
             return;
         }
     }
     // team sizes: level 2 {4, 8} lanes per patch (P->rp_ts2), level 3 {8, 16}
     if (layer == 2) {
         if (P->rp_ts2 >= 8)
-            launch_rowpair<T, 2, MODE, PREC, 8>(P, a.uin, a.uout, a.xdone);
+            launch_rowpair<T, 2, MODE, PREC, 8>(P, a.uin, a.uout);
         else
-            launch_rowpair<T, 2, MODE, PREC, 4>(P, a.uin, a.uout, a.xdone);
+            launch_rowpair<T, 2, MODE, PREC, 4>(P, a.uin, a.uout);
     } else {
         if (P->ts3 >= 16)
-            launch_rowpair<T, 3, MODE, PREC, 16>(P, a.uin, a.uout, a.xdone);
+            launch_rowpair<T, 3, MODE, PREC, 16>(P, a.uin, a.uout);
         else
-            launch_rowpair<T, 3, MODE, PREC, 8>(P, a.uin, a.uout, a.xdone);
+            launch_rowpair<T, 3, MODE, PREC, 8>(P, a.uin, a.uout);
     }
 }
 
@@ -512,25 +517,24 @@ void dispatch_fused(cmg_plan* P, int layer, const FusedArgs<T>& a) {
         launch_coarse<T, 3, MODE, PREC>(P, a);
 }
 
-// one fused level visit uin -> uout; xdone: copy source of stopped images
-// (nullptr: uin); efuse_prev != nullptr: energy-fused level-1 visit whose
-// input is the cycle input u_g and efuse_prev is u_{g-1}
+
+// one fused level visit uin -> uout; efuse_prev != nullptr: energy-fused
+// level-1 visit whose input is the cycle input u_g and efuse_prev is u_{g-1}
 template <typename T>
-void enqueue_fused_level_x(cmg_plan* P, int layer, const void* uin, void* uout, const void* xdone,
-                           const void* efuse_prev, bool has_ref) {
+void enqueue_fused_level_x(cmg_plan* P, int layer, const void* uin, void* uout, const void* efuse_prev,
+                           bool has_ref) {
     const Level& L = P->lv[layer];
     FusedArgs<T> a;
     memset(&a, 0, sizeof(a));
     a.uin = (const T*)uin;
     a.uout = (T*)uout;
-    a.xdone = (const T*)(xdone ? xdone : uin);
     a.efuse = efuse_prev != nullptr;
     if (a.efuse) {
         a.uprev = (const T*)efuse_prev;
         a.ref = has_ref ? (const T*)P->ref : nullptr;
         a.partials = P->partials;
         a.mode = P->mode;
-        a.fz = make_energy_fin(P, make_trace_args(P, nullptr, nullptr), 2);
+        a.fz = make_energy_fin(P, make_trace_args(P, nullptr, nullptr), 2, buf_index(P, uin));
     }
     a.f = (const T*)P->f;
     a.istride = P->N;
@@ -563,7 +567,7 @@ void enqueue_fused_level_x(cmg_plan* P, int layer, const void* uin, void* uout, 
 
 template <typename T>
 void enqueue_fused_level(cmg_plan* P, int layer, const void* uin, void* uout) {
-    enqueue_fused_level_x<T>(P, layer, uin, uout, nullptr, nullptr, false);
+    enqueue_fused_level_x<T>(P, layer, uin, uout, nullptr, false);
 }
 
 // Two V-cycles per graph body with a 3-buffer rotation: fused levels write
@@ -631,8 +635,7 @@ void enqueue_body_efused(cmg_plan* P, int full, bool has_ref) {
         for (int j : seq) {
             if (fusedj(j)) {
                 const int out = first ? Z : ((cur == Z) ? Pv : Z);
-                enqueue_fused_level_x<T>(P, j, P->ubuf[cur], P->ubuf[out], P->ubuf[X], first ? P->ubuf[Pv] : nullptr,
-                                         has_ref);
+                enqueue_fused_level_x<T>(P, j, P->ubuf[cur], P->ubuf[out], first ? P->ubuf[Pv] : nullptr, has_ref);
                 first = false;
                 cur = out;
             } else {
@@ -646,6 +649,14 @@ void enqueue_body_efused(cmg_plan* P, int full, bool has_ref) {
         X = cur;
         Z = 3 - X - Pv;
     }
+}
+
+template <typename T>
+void enqueue_collect(cmg_plan* P) {
+    const int blocks = (int)std::min<long long>((P->N + 255) / 256, 1024);
+    klaunch(P, k_collect<T>, dim3(blocks, P->B), 256, 0, (T*)P->ubuf[0], (const T*)P->ubuf[1], (const T*)P->ubuf[2],
+            P->N, (const ImgState*)P->st);
+    P->enq += 1;
 }
 
 template <typename T>
@@ -696,6 +707,7 @@ int energy_bulk_cfg_impl(int batch, int m, int n, int px, int ns, int* H_out) {
                                               long long, long long);                                   \
     template void cmg::enqueue_body_fused<T>(cmg_plan*, int, bool);                  \
     template void cmg::enqueue_body_efused<T>(cmg_plan*, int, bool);                 \
+    template void cmg::enqueue_collect<T>(cmg_plan*);                                \
     template <>                                                                     \
     int cmg::coarse_region<T>(int layer) {                                          \
         return cmg::coarse_region_impl<T>(layer);                                   \

@@ -168,6 +168,8 @@ template <typename T>
 void enqueue_body_fused(cmg_plan* P, int full, bool has_ref);
 template <typename T>
 void enqueue_body_efused(cmg_plan* P, int full, bool has_ref);
+template <typename T>
+void enqueue_collect(cmg_plan* P);
 inline int efused_out(const cmg_plan* P, int full, int X, int Pv, int Z) {
     int cur = X;
     bool first = true;

@@ -33,7 +33,6 @@ template <typename T>
 struct RowPairArgs {
     const T* X;      // level input (u before this level)
     T* Y;            // level output
-    const T* Xdone;  // stopped images: copy source (the cycle input in the energy-fused cycle, else X)
     int ntiles;      // column tiles per patch row
     int nj;          // patch columns
     SweepArgs<T> c0, c1;  // colours (p,0) and (p,1): p, q, hc, wc, flat, single, backward constants
@@ -262,29 +261,13 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// stopped image: carry the owned pixels along the buffer rotation
-template <typename T, int LAYER, int TS, int NT>
-__device__ __forceinline__ void rp_copy_owned(const RowPairArgs<T>& a, const RPItem<T>& it) {
-    using G = RowPairGeom<LAYER, TS, NT>;
-    const int n = a.c0.n;
-    const T* xd = a.Xdone + (long long)it.b * a.c0.istride;
-    for (int i = it.R0; i < it.orow1; ++i)
-        for (int k = it.ok0 + threadIdx.x; k < it.ok1; k += G::NT) {
-            const long long g = (long long)i * n + k;
-            it.Yb[g] = xd[g];
-        }
-}
-
 template <typename T, int LAYER, int MODE, int PREC, int TS, int NT = 256>
 __global__ void __launch_bounds__(NT) k_rowpair(RowPairArgs<T> a) {
     pdl_sync();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* win = reinterpret_cast<T*>(smem_raw);
     const RPItem<T> it = rp_item<T, LAYER, TS, NT>(a, blockIdx.z, blockIdx.y, blockIdx.x);
-    if (a.c0.st[it.b].done) {
-        rp_copy_owned<T, LAYER, TS, NT>(a, it);
-        return;
-    }
+    if (a.c0.st[it.b].done) return;  // stopped image (final u in ImgState::final_buf)
     rp_stage<T, LAYER, TS, NT>(a, it, win);
     __syncthreads();
     rp_compute<T, LAYER, MODE, PREC, TS, NT>(a, it, win);
@@ -375,9 +358,7 @@ __global__ void __launch_bounds__(NT) k_rowpair_bulk(RowPairArgs<T> a, int rows,
         }
         mbar_wait(&full[st], (unsigned)((i / STAGES) & 1));
         T* win = stage0 + st * STAGE;
-        if (a.c0.st[cur.b].done) {
-            rp_copy_owned<T, LAYER, 1, NT>(a, cur);
-        } else {
+        if (!a.c0.st[cur.b].done) {
             rp_compute<T, LAYER, MODE_MEAN, PREC_FAST, 1, NT, A, true>(a, cur, win);
             if (tid == 0) store(cur, win);
         }

@@ -9,7 +9,7 @@ for e in "$@"; do
 import json, sys
 try:
     d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
-    print(f"{sys.argv[2]:40s} ms={d['ms_per_step']:.3f} levels={ {k: round(v*1000,1) for k,v in d['config'].get('level_sweep_ms',{}).items()} }")
+    print(f"{sys.argv[2]:40s} ms={d['ms_per_step']:.3f} levels={ {k: round(v*1000,1) for k,v in d.get('detail', d['config']).get('level_sweep_ms',{}).items()} }")
 except Exception as ex:
     print(sys.argv[2], "FAILED", ex)
 PY
