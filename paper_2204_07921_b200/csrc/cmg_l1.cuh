@@ -208,28 +208,36 @@ template <typename T, int TH, int TW>
 __device__ __forceinline__ void l1_energy_sums(const T* su, const T* sf, int R, int C, int m, int n, const T* up,
                                                const T* rf, int mode, double* partials, int b, int cta, int nbx) {
     using G = L1Geom<T, TH, TW>;
+    // owned pixels plane by plane (colour class (P,Q) of the quad-planar layout):
+    // every neighbour is a compile-time offset from one shared-memory base
+    constexpr int PH = TH / 2, PW = TW / 2, CNT = PH * PW;
+    static_assert(G::HALO % 2 == 0, "owned pixels start on an even region row");
     double acc[NSUM] = {0, 0, 0, 0, 0};
-    for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
-        const int i = e / TW, k = e % TW;
-        const int gi = R + i, gk = C + k;
-        if (gi >= m || gk >= n) continue;
-        const int ri = i + G::HALO, rk = k + G::HALO;
-        const T c = su[G::idx(ri, rk)];
-        const T t = curv_term<T>(c, su[G::idx(ri, rk + 1)], su[G::idx(ri, rk - 1)], su[G::idx(ri - 1, rk)],
-                                 su[G::idx(ri + 1, rk)], su[G::idx(ri - 1, rk + 1)], su[G::idx(ri + 1, rk - 1)],
-                                 su[G::idx(ri - 1, rk - 1)], su[G::idx(ri + 1, rk + 1)], mode);
-        const long long g = (long long)gi * n + gk;
-        const double c64 = (double)c;
-        const double d = c64 - (double)sf[G::idx(ri, rk)];
-        acc[0] += (double)t;
-        acc[1] += d * d;
-        acc[2] += fabs(c64 - (double)up[g]);
-        acc[3] += fabs(c64);
-        if (rf) {
-            const double dr = c64 - (double)rf[g];
-            acc[4] += dr * dr;
+    static_for<0, 4>([&](auto cp) {
+        constexpr int P = decltype(cp)::value >> 1, Q = decltype(cp)::value & 1;
+#pragma unroll 1
+        for (int t = threadIdx.x; t < CNT; t += blockDim.x) {
+            const int ii = t / PW, kk = t % PW;
+            const int gi = R + 2 * ii + P, gk = C + 2 * kk + Q;
+            if (gi >= m || gk >= n) continue;
+            const QuadAcc<T, TH, TW, P, Q> A{su, G::HALO / 2 + ii, G::HALO / 2 + kk};
+            const T c = A.template at<0, 0>();
+            const T tm = curv_term<T>(c, A.template at<0, 1>(), A.template at<0, -1>(), A.template at<-1, 0>(),
+                                      A.template at<1, 0>(), A.template at<-1, 1>(), A.template at<1, -1>(),
+                                      A.template at<-1, -1>(), A.template at<1, 1>(), mode);
+            const long long g = (long long)gi * n + gk;
+            const double c64 = (double)c;
+            const double d = c64 - (double)sf[(P * 2 + Q) * G::PLANE + (G::HALO / 2 + ii) * G::QW + G::HALO / 2 + kk];
+            acc[0] += (double)tm;
+            acc[1] += d * d;
+            acc[2] += fabs(c64 - (double)up[g]);
+            acc[3] += fabs(c64);
+            if (rf) {
+                const double dr = c64 - (double)rf[g];
+                acc[4] += dr * dr;
+            }
         }
-    }
+    });
     cta_sums_store(acc, partials, nbx, cta, b);
 }
 
