@@ -36,6 +36,8 @@ VARIANTS = {
     "no_programmatic_launch": {"CMG_PDL": "0"},
     "level1_wide_tiles": {"CMG_L1_WIDE": "1"},
     "energy_256_threads": {"CMG_ENERGY_NT": "256"},
+    "energy_separate_pass": {"CMG_EFUSE": "0"},
+    "energy_separate_pass_per_colour": {"CMG_EFUSE": "0", "CMG_ROWPAIR": "0"},
 }
 
 SCRIPT = r"""
