@@ -489,16 +489,7 @@ void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
             return;
         }
     }
-    // team sizes: level 2 {1, 4, 8} lanes per patch (P->rp_ts2), level 3 {1, 8, 16}
-    // (1: one thread per patch, compile-time plane offsets)
-    if (layer == 2 && P->rp_ts2 == 1) {
-        launch_rowpair<T, 2, MODE, PREC, 1, 128>(P, a.uin, a.uout);
-        return;
-    }
-    if (layer == 3 && P->ts3 == 1) {
-        launch_rowpair<T, 3, MODE, PREC, 1, 32>(P, a.uin, a.uout);
-        return;
-    }
+    // team sizes: level 2 {4, 8} lanes per patch (P->rp_ts2), level 3 {8, 16}
     if (layer == 2) {
         if (P->rp_ts2 >= 8)
             launch_rowpair<T, 2, MODE, PREC, 8>(P, a.uin, a.uout);

@@ -213,11 +213,7 @@ __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem
             const int C0 = Jc * S;
             const double* fsp =
                 A.fsum ? A.fsum + (long long)it.b * A.fs_img + (long long)(R0 / S) * A.fs_ld + Jc : nullptr;
-            T c;
-            if constexpr (TS == 1 && !(MODE == MODE_MEAN && PREC == PREC_FAST))
-                c = patch_solve_ct<T, LAYER, MODE, PREC>(U, F, R0, C0, A);  // compile-time plane offsets
-            else
-                c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, A, fsp);
+            const T c = patch_solve_team<T, LAYER, MODE, PREC, TS>(U, F, R0, C0, lane, A, fsp);
             if (active) {
                 if (lane == 0 && !isfinite(c)) bad = true;
                 // prolongation u += c on the patch's in-image pixels (hierarchy.py:117-126);
