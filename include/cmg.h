@@ -49,6 +49,8 @@ typedef struct cmg_plan cmg_plan;
 /* library version (major*10000 + minor*100 + patch) */
 int cmg_version(void);
 
+typedef struct cmg_mplan cmg_mplan;
+
 /* message of the last error on this thread ("" if none) */
 const char* cmg_last_error(void);
 
@@ -123,7 +125,8 @@ int cmg_time_sweep(cmg_plan* plan, int layer, int color, int reps, double* ms_pe
 /*
  * Building blocks for host-driven decompositions (horizontal strips over
  * several GPUs, paper_2204_07921_b200/strips.py).  A plan owns five device
- * buffers: 0..2 = the u rotation buffers, 3 = f, 4 = reference image.
+ * buffers: 0..2 = the u rotation buffers, 3 = f, 4 = reference image; index
+ * 5 is the batch x 6 doubles of cmg_strip_partials_async.
  */
 /* device pointer of buffer `index` (batch*m*n elements) */
 int cmg_plan_buffer(cmg_plan* plan, int index, void** dev_ptr);
@@ -138,6 +141,43 @@ int cmg_level_step(cmg_plan* plan, int layer, int in_index, int out_index, doubl
  *  sum (u-ref)^2}; F = s0 + (alpha/2) s1 as in tangent.energy (tangent.py:339-341) */
 int cmg_energy_partials(cmg_plan* plan, int u_index, int prev_index, int use_ref, int row_lo, int row_hi,
                         double* out);
+
+/*
+ * Asynchronous strip cycle (one host synchronisation per V-cycle): everything
+ * below only ENQUEUES on the plan's CUDA stream (cmg_plan_stream), so ghost-row
+ * exchanges and all-reduces issued on that stream (NCCL / P2P copies) order
+ * behind the level steps without host round trips.
+ *   cmg_strip_begin           backward-step constants + per-image state reset
+ *   cmg_level_step_async      cmg_level_step without the synchronisation
+ *   cmg_strip_partials_async  energy sums of rows [row_lo,row_hi) -> device
+ *                             buffer 5: batch x 5 sums, then batch
+ *                             non-finite-correction flags (6 doubles for one
+ *                             image; all-reduce it in place)
+ *   cmg_strip_read            device buffer 5 -> host (6 x batch doubles), synchronises
+ */
+int cmg_plan_stream(cmg_plan* plan, void** stream);
+
+/*
+ * Multi-device batch plan: a batch of same-shape images sharded data-parallel
+ * over n_devices GPUs (device_ids; an id may repeat: independent plans on one
+ * GPU).  Device d gets a contiguous slice of images (sizes differ by <= 1);
+ * cmg_mplan_solve runs the shards concurrently (one host thread per shard,
+ * no collective: images are independent) with cmg_solve's arguments and
+ * output layout for the WHOLE batch, and returns the first non-OK status
+ * in image order.  The reference parallelises inside denoise
+ * (driver.py:279-280); this is the library-level equivalent for batches.
+ */
+int cmg_mplan_create(cmg_mplan** out, int m, int n, int batch, int layers, int mode, int dtype, int precision,
+                     const int* device_ids, int n_devices);
+int cmg_mplan_destroy(cmg_mplan* mplan);
+int cmg_mplan_solve(cmg_mplan* mplan, const void* f_host, const void* ref_host, void* u_host_out, double alpha,
+                    double epsilon, int max_outer, int inner_iters, int stop_rule, int full_vcycle, double peak,
+                    double* energy, double* rel_energy, double* rel_u, double* psnr, double* seconds, int* iterations,
+                    int* status);
+int cmg_strip_begin(cmg_plan* plan, double alpha, int inner_iters);
+int cmg_level_step_async(cmg_plan* plan, int layer, int in_index, int out_index);
+int cmg_strip_partials_async(cmg_plan* plan, int u_index, int prev_index, int use_ref, int row_lo, int row_hi);
+int cmg_strip_read(cmg_plan* plan, double* out);
 
 /*
  * curvemg.image.ssim (image.py:152-192) on the GPU, bit-identical: mean SSIM

@@ -25,6 +25,8 @@ SYMBOLS = (
     "cmg_solve_device", "cmg_sweep_layer", "cmg_energy", "cmg_plane_table", "cmg_plan_stats", "cmg_time_sweep",
     "cmg_host_alloc", "cmg_host_free", "cmg_plan_buffer", "cmg_buffer_upload", "cmg_buffer_download",
     "cmg_level_step", "cmg_energy_partials", "cmg_ssim_batch", "cmg_plan_ssim", "cmg_l2_read_bandwidth",
+    "cmg_plan_stream", "cmg_strip_begin", "cmg_level_step_async", "cmg_strip_partials_async", "cmg_strip_read",
+    "cmg_mplan_create", "cmg_mplan_destroy", "cmg_mplan_solve",
 )
 
 
@@ -69,6 +71,22 @@ def _declare(L):
     L.cmg_time_sweep.argtypes = [_vp, _i, _i, _i, _dp]
     L.cmg_host_alloc.restype = _vp
     L.cmg_host_alloc.argtypes = [ctypes.c_ulonglong]
+    L.cmg_mplan_create.restype = _i
+    L.cmg_mplan_create.argtypes = [ctypes.POINTER(_vp), _i, _i, _i, _i, _i, _i, _i, _ip, _i]
+    L.cmg_mplan_destroy.restype = _i
+    L.cmg_mplan_destroy.argtypes = [_vp]
+    L.cmg_mplan_solve.restype = _i
+    L.cmg_mplan_solve.argtypes = solve_args
+    L.cmg_plan_stream.restype = _i
+    L.cmg_plan_stream.argtypes = [_vp, ctypes.POINTER(_vp)]
+    L.cmg_strip_begin.restype = _i
+    L.cmg_strip_begin.argtypes = [_vp, _d, _i]
+    L.cmg_level_step_async.restype = _i
+    L.cmg_level_step_async.argtypes = [_vp, _i, _i, _i]
+    L.cmg_strip_partials_async.restype = _i
+    L.cmg_strip_partials_async.argtypes = [_vp, _i, _i, _i, _i, _i]
+    L.cmg_strip_read.restype = _i
+    L.cmg_strip_read.argtypes = [_vp, _dp]
     L.cmg_l2_read_bandwidth.restype = _i
     L.cmg_l2_read_bandwidth.argtypes = [_i, ctypes.c_longlong, _i, _dp]
     L.cmg_host_free.restype = _i
@@ -182,3 +200,33 @@ def l2_read_bandwidth(device: int = 0, nbytes: int = 32 << 20, reps: int = 50) -
     if rc != CMG_OK:
         raise RuntimeError(last_error())
     return out.value
+
+
+class MPlan:
+    """cmg_mplan: one batch sharded over several devices (ids may repeat)."""
+
+    def __init__(self, m: int, n: int, batch: int, layers: int, mode: str, dtype: str, precision: str, devices):
+        devs = (ctypes.c_int * len(devices))(*devices)
+        h = _vp()
+        rc = lib().cmg_mplan_create(ctypes.byref(h), m, n, batch, layers, MODE[mode], DTYPE[dtype], PREC[precision],
+                                    devs, len(devices))
+        if rc != CMG_OK:
+            msg = last_error()
+            if rc == CMG_EINVAL:
+                raise ValueError(msg)
+            raise RuntimeError(f"cmg_mplan_create failed ({rc}): {msg}")
+        self.handle = h
+        self.devices = tuple(devices)
+        self.shape = (batch, m, n)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().cmg_mplan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+

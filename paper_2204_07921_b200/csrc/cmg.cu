@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cmg.h"
@@ -213,6 +214,36 @@ int ensure_trace(cmg_plan* P, int cap) {
         P->gkey = -1;
     }
     return CMG_OK;
+}
+
+// one level visit in_index -> out_index on the plan stream (strip steps):
+// the fused tile / row-parity kernel, or a copy + the in-place colour sweeps
+void enqueue_level(cmg_plan* P, int layer, int in_index, int out_index) {
+    const bool fusedj = P->fused && layer <= 3 && ((P->fuse_mask >> (layer - 1)) & 1);
+    if (fusedj) {
+        if (P->dtype == CMG_F64)
+            enqueue_fused_level<double>(P, layer, P->ubuf[in_index], P->ubuf[out_index]);
+        else
+            enqueue_fused_level<float>(P, layer, P->ubuf[in_index], P->ubuf[out_index]);
+        return;
+    }
+    cudaMemcpyAsync(P->ubuf[out_index], P->ubuf[in_index], P->esz * (size_t)P->N * P->B, cudaMemcpyDeviceToDevice,
+                    P->stream);
+    void* save = P->u;
+    P->u = P->ubuf[out_index];
+    for (int c = 0; c < 4; ++c) {
+        if (P->dtype == CMG_F64)
+            enqueue_sweep<double>(P, layer, c);
+        else
+            enqueue_sweep<float>(P, layer, c);
+    }
+    P->u = save;
+}
+
+// strip mode: per-image non-finite-correction flag next to the 5 energy sums
+__global__ void k_strip_flags(const ImgState* st, double* raw6, int B) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < B) raw6[(long long)B * NSUM + b] = st[b].bad ? 1.0 : 0.0;
 }
 
 int check_cfg(double alpha, double eps, int max_outer, int inner, int stop_rule) {
@@ -673,7 +704,7 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     CKP(cudaMalloc(&P->ndone, sizeof(int) * 2));
     P->iters = P->ndone + 1;
     CKP(cudaMalloc(&P->eonly, sizeof(double) * batch));
-    CKP(cudaMalloc(&P->raw5, sizeof(double) * NSUM * batch));
+    CKP(cudaMalloc(&P->raw5, sizeof(double) * (NSUM + 1) * batch));  // strip mode: 5 sums + flag per image
     CKP(cudaMalloc(&P->tickets, sizeof(int) * (batch + 1)));
     CKP(cudaMemset(P->tickets, 0, sizeof(int) * (batch + 1)));
     if (const char* pd = getenv("CMG_PDL")) P->pdl = atoi(pd) != 0;
@@ -861,6 +892,7 @@ int cmg_time_sweep(cmg_plan* P, int layer, int color, int reps, double* ms_per_l
 static void* buffer_ptr(cmg_plan* P, int index) {
     if (index >= 0 && index <= 2) return P->ubuf[index];
     if (index == 3) return P->f;
+    if (index == 5) return P->raw5;
     if (index == 4) {
         if (!P->ref) cudaMalloc(&P->ref, P->esz * (size_t)P->N * P->B);
         return P->ref;
@@ -967,6 +999,7 @@ int cmg_plan_ssim(cmg_plan* P, int a_index, int b_index, const double* window, d
     int rc = set_device(P);
     if (rc) return rc;
     if (P->m < 11 || P->n < 11) return fail(CMG_EINVAL, "image smaller than the 11x11 SSIM window");
+    if (a_index < 0 || a_index > 4 || b_index < 0 || b_index > 4) return fail(CMG_EINVAL, "buffer index must be 0..4");
     const void* a = buffer_ptr(P, a_index);
     const void* b = buffer_ptr(P, b_index);
     if (!a || !b) return fail(CMG_EINVAL, "buffer index must be 0..4");
@@ -985,6 +1018,7 @@ int cmg_plan_buffer(cmg_plan* P, int index, void** dev_ptr) {
 
 int cmg_buffer_upload(cmg_plan* P, int index, const void* host) {
     if (!P || !host) return fail(CMG_EINVAL, "NULL argument");
+    if (index < 0 || index > 4) return fail(CMG_EINVAL, "buffer index must be 0..4");
     int rc = set_device(P);
     if (rc) return rc;
     void* p = buffer_ptr(P, index);
@@ -1005,6 +1039,7 @@ int cmg_buffer_upload(cmg_plan* P, int index, const void* host) {
 
 int cmg_buffer_download(cmg_plan* P, int index, void* host) {
     if (!P || !host) return fail(CMG_EINVAL, "NULL argument");
+    if (index < 0 || index > 4) return fail(CMG_EINVAL, "buffer index must be 0..4");
     int rc = set_device(P);
     if (rc) return rc;
     void* p = buffer_ptr(P, index);
@@ -1028,25 +1063,7 @@ int cmg_level_step(cmg_plan* P, int layer, int in_index, int out_index, double a
     P->hostP = sp;
     CK(cudaMemcpyAsync(P->P, &sp, sizeof(sp), cudaMemcpyHostToDevice, P->stream));
     CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
-    const bool fusedj = P->fused && layer <= 3 && ((P->fuse_mask >> (layer - 1)) & 1);
-    if (fusedj) {
-        if (P->dtype == CMG_F64)
-            enqueue_fused_level<double>(P, layer, P->ubuf[in_index], P->ubuf[out_index]);
-        else
-            enqueue_fused_level<float>(P, layer, P->ubuf[in_index], P->ubuf[out_index]);
-    } else {
-        CK(cudaMemcpyAsync(P->ubuf[out_index], P->ubuf[in_index], P->esz * (size_t)P->N * P->B,
-                           cudaMemcpyDeviceToDevice, P->stream));
-        void* save = P->u;
-        P->u = P->ubuf[out_index];
-        for (int c = 0; c < 4; ++c) {
-            if (P->dtype == CMG_F64)
-                enqueue_sweep<double>(P, layer, c);
-            else
-                enqueue_sweep<float>(P, layer, c);
-        }
-        P->u = save;
-    }
+    enqueue_level(P, layer, in_index, out_index);
     CK(cudaGetLastError());
     std::vector<ImgState> hs(P->B);
     CK(cudaMemcpyAsync(hs.data(), P->st, sizeof(ImgState) * P->B, cudaMemcpyDeviceToHost, P->stream));
@@ -1111,6 +1128,150 @@ int cmg_l2_read_bandwidth(int device, long long bytes, int reps, double* gbs) {
     cudaFree(sink);
     if (e != cudaSuccess) return fail(CMG_ECUDA, cudaGetErrorString(e));
     *gbs = (double)n16 * 16.0 * reps / (ms * 1e-3) / 1e9;
+    return CMG_OK;
+}
+
+int cmg_plan_stream(cmg_plan* P, void** stream) {
+    if (!P || !stream) return fail(CMG_EINVAL, "NULL argument");
+    *stream = (void*)P->stream;
+    return CMG_OK;
+}
+
+int cmg_strip_begin(cmg_plan* P, double alpha, int inner_iters) {
+    if (!P) return fail(CMG_EINVAL, "plan is NULL");
+    int rc = check_cfg(alpha, 1.0, 1, inner_iters, 0);
+    if (rc) return rc;
+    rc = set_device(P);
+    if (rc) return rc;
+    SolveParams sp;
+    fill_params(P, sp, alpha, 1.0, 1, inner_iters, 0, false, 1.0);
+    P->hostP = sp;
+    CK(cudaMemcpyAsync(P->P, &sp, sizeof(sp), cudaMemcpyHostToDevice, P->stream));
+    CK(cudaMemsetAsync(P->st, 0, sizeof(ImgState) * P->B, P->stream));
+    // the host struct must outlive the async copy: make this call synchronous once
+    CK(cudaStreamSynchronize(P->stream));
+    return CMG_OK;
+}
+
+int cmg_level_step_async(cmg_plan* P, int layer, int in_index, int out_index) {
+    if (!P) return fail(CMG_EINVAL, "plan is NULL");
+    if (layer < 1 || layer > P->layers) return fail(CMG_EINVAL, "layer outside the plan's hierarchy");
+    if (in_index < 0 || in_index > 2 || out_index < 0 || out_index > 2 || in_index == out_index)
+        return fail(CMG_EINVAL, "in/out must be distinct rotation buffers 0..2");
+    int rc = set_device(P);
+    if (rc) return rc;
+    enqueue_level(P, layer, in_index, out_index);
+    CK(cudaGetLastError());
+    return CMG_OK;
+}
+
+int cmg_strip_partials_async(cmg_plan* P, int u_index, int prev_index, int use_ref, int row_lo, int row_hi) {
+    if (!P) return fail(CMG_EINVAL, "plan is NULL");
+    if (u_index < 0 || u_index > 2 || prev_index < 0 || prev_index > 2) return fail(CMG_EINVAL, "bad buffer index");
+    if (row_lo < 0 || row_hi > P->m || row_lo > row_hi) return fail(CMG_EINVAL, "bad row range");
+    if (use_ref && !P->ref) return fail(CMG_EINVAL, "no reference uploaded (buffer 4)");
+    int rc = set_device(P);
+    if (rc) return rc;
+    const long long lo = (long long)row_lo * P->n, hi = (long long)row_hi * P->n;
+    if (P->dtype == CMG_F64)
+        enqueue_energy_ptrs<double>(P, P->ubuf[u_index], P->ubuf[prev_index], use_ref != 0, nullptr, 0, P->raw5, lo, hi);
+    else
+        enqueue_energy_ptrs<float>(P, P->ubuf[u_index], P->ubuf[prev_index], use_ref != 0, nullptr, 0, P->raw5, lo, hi);
+    k_strip_flags<<<(P->B + 127) / 128, 128, 0, P->stream>>>(P->st, P->raw5, P->B);
+    CK(cudaGetLastError());
+    return CMG_OK;
+}
+
+int cmg_strip_read(cmg_plan* P, double* out) {
+    if (!P || !out) return fail(CMG_EINVAL, "NULL argument");
+    int rc = set_device(P);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(out, P->raw5, sizeof(double) * (NSUM + 1) * P->B, cudaMemcpyDeviceToHost, P->stream));
+    CK(cudaStreamSynchronize(P->stream));
+    return CMG_OK;
+}
+
+}  // extern "C"
+
+struct cmg_mplan {
+    int m = 0, n = 0, B = 0, esz = 8;
+    std::vector<cmg_plan*> plans;
+    std::vector<int> off, cnt;
+};
+
+extern "C" {
+
+int cmg_mplan_destroy(cmg_mplan* M) {
+    if (!M) return CMG_OK;
+    for (cmg_plan* p : M->plans) cmg_plan_destroy(p);
+    delete M;
+    return CMG_OK;
+}
+
+int cmg_mplan_create(cmg_mplan** out, int m, int n, int batch, int layers, int mode, int dtype, int precision,
+                     const int* device_ids, int n_devices) {
+    if (!out) return fail(CMG_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!device_ids || n_devices < 1) return fail(CMG_EINVAL, "need at least one device id");
+    if (batch < n_devices) return fail(CMG_EINVAL, "batch must be at least the number of devices");
+    cmg_mplan* M = new cmg_mplan();
+    M->m = m;
+    M->n = n;
+    M->B = batch;
+    M->esz = dtype == CMG_F64 ? 8 : 4;
+    int o = 0;
+    for (int d = 0; d < n_devices; ++d) {
+        const int c = batch / n_devices + (d < batch % n_devices ? 1 : 0);
+        cmg_plan* p = nullptr;
+        const int rc = cmg_plan_create(&p, m, n, c, layers, mode, dtype, precision, device_ids[d]);
+        if (rc != CMG_OK) {
+            cmg_mplan_destroy(M);
+            return rc;
+        }
+        M->plans.push_back(p);
+        M->off.push_back(o);
+        M->cnt.push_back(c);
+        o += c;
+    }
+    *out = M;
+    return CMG_OK;
+}
+
+int cmg_mplan_solve(cmg_mplan* M, const void* f_host, const void* ref_host, void* u_host_out, double alpha,
+                    double epsilon, int max_outer, int inner_iters, int stop_rule, int full_vcycle, double peak,
+                    double* energy, double* rel_energy, double* rel_u, double* psnr, double* seconds, int* iterations,
+                    int* status) {
+    if (!M) return fail(CMG_EINVAL, "plan is NULL");
+    if (!f_host) return fail(CMG_EINVAL, "f is NULL");
+    const int nd = (int)M->plans.size();
+    const size_t img = (size_t)M->m * M->n * M->esz;
+    const size_t cap = (size_t)max_outer + 1;
+    std::vector<int> rcs(nd, CMG_OK);
+    std::vector<std::string> errs(nd);
+    std::vector<int> st(M->B, CMG_OK);
+    auto shard = [&](int d) {
+        const size_t o = (size_t)M->off[d];
+        auto tr = [&](double* a) { return a ? a + o * cap : nullptr; };
+        rcs[d] = cmg_solve(M->plans[d], (const char*)f_host + o * img, ref_host ? (const char*)ref_host + o * img : nullptr,
+                           u_host_out ? (char*)u_host_out + o * img : nullptr, alpha, epsilon, max_outer, inner_iters,
+                           stop_rule, full_vcycle, peak, tr(energy), tr(rel_energy), tr(rel_u), tr(psnr), tr(seconds),
+                           iterations ? iterations + o : nullptr, st.data() + o);
+        if (rcs[d] == CMG_EINVAL || rcs[d] == CMG_ECUDA) errs[d] = g_err;
+    };
+    std::vector<std::thread> th;
+    for (int d = 1; d < nd; ++d) th.emplace_back(shard, d);
+    shard(0);
+    for (auto& t : th) t.join();
+    for (int d = 0; d < nd; ++d)
+        if (rcs[d] == CMG_EINVAL || rcs[d] == CMG_ECUDA) return fail(rcs[d], errs[d]);
+    if (status)
+        for (int b = 0; b < M->B; ++b) status[b] = st[b];
+    for (int b = 0; b < M->B; ++b)
+        if (st[b] != CMG_OK) {
+            if (st[b] == CMG_DIVERGED) g_err = "objective became non-finite";
+            if (st[b] == CMG_ENONFINITE) g_err = "corrections must be finite";
+            return st[b];
+        }
     return CMG_OK;
 }
 

@@ -238,10 +238,29 @@ def _raise_for(rc: int):
         raise RuntimeError(f"CUDA failure in libcmg: {msg}")
 
 
-def _solve(fs: np.ndarray, refs, cfg: SolverConfig, peak: float):
-    """Run cmg_solve on a (B, m, n) host stack; returns (u, traces, statuses, plan)."""
+def get_mplan(m: int, n: int, batch: int, cfg: SolverConfig, devices) -> N.MPlan:
+    """Per-thread cache of multi-device batch plans (cmg_mplan)."""
+    plans = getattr(_tls, "mplans", None)
+    if plans is None:
+        plans = _tls.mplans = {}
+    key = (m, n, batch, cfg.layers, cfg.mode, cfg.dtype, cfg.precision, tuple(devices))
+    p = plans.get(key)
+    if p is None:
+        if len(plans) >= _PLAN_CAP:
+            for k in list(plans)[: _PLAN_CAP // 2]:
+                plans.pop(k).close()
+        p = N.MPlan(m, n, batch, cfg.layers, cfg.mode, cfg.dtype, cfg.precision, list(devices))
+        plans[key] = p
+    return p
+
+
+def _solve(fs: np.ndarray, refs, cfg: SolverConfig, peak: float, devices=None):
+    """Run cmg_solve (or cmg_mplan_solve over ``devices``) on a (B, m, n) host
+    stack; returns (u, traces, statuses, plan)."""
     B, m, n = fs.shape
-    plan = get_plan(m, n, B, cfg)
+    multi = devices is not None and len(devices) > 0
+    plan = get_mplan(m, n, B, cfg, devices) if multi else get_plan(m, n, B, cfg)
+    solve = N.lib().cmg_mplan_solve if multi else N.lib().cmg_solve
     dt = _np_dtype(cfg)
     f_in = np.ascontiguousarray(fs, dtype=dt)
     r_in = None if refs is None else np.ascontiguousarray(refs, dtype=dt)
@@ -250,7 +269,7 @@ def _solve(fs: np.ndarray, refs, cfg: SolverConfig, peak: float):
     tr = {k: np.full((B, cap), np.nan) for k in ("energy", "rel_e", "rel_u", "psnr", "sec")}
     its = np.zeros(B, dtype=np.int32)
     sts = np.zeros(B, dtype=np.int32)
-    rc = N.lib().cmg_solve(plan.handle, N.ptr(f_in), N.ptr(r_in), N.ptr(u), cfg.alpha, cfg.epsilon,
+    rc = solve(plan.handle, N.ptr(f_in), N.ptr(r_in), N.ptr(u), cfg.alpha, cfg.epsilon,
                            cfg.max_outer, cfg.inner_iters, N.STOP[cfg.stop_rule], int(cfg.full_vcycle), peak,
                            N.dptr(tr["energy"]), N.dptr(tr["rel_e"]), N.dptr(tr["rel_u"]), N.dptr(tr["psnr"]),
                            N.dptr(tr["sec"]), N.iptr(its), N.iptr(sts))
@@ -294,11 +313,14 @@ def denoise(f: Image, config, reference: Image | None = None) -> tuple[Image, Co
     return Image._from_solver(u[0], f.peak), traces[0]
 
 
-def denoise_batch(fs, config, references=None, peak: float | None = None):
+def denoise_batch(fs, config, references=None, peak: float | None = None, devices=None):
     """Denoise B same-shape images in one launch sequence (per-image stopping).
 
     ``fs`` is a list of Images or a (B, m, n) array; returns a list of
     (Image, ConvergenceTrace).  Divergent images raise like ``denoise``.
+    ``devices`` (list of CUDA ordinals, may repeat) shards the batch
+    data-parallel over those GPUs (cmg_mplan: contiguous image slices, one
+    host thread per shard, no collective); results are identical to one plan.
     """
     cfg = _coerce_config(config)
     if isinstance(fs, np.ndarray):
@@ -313,7 +335,7 @@ def denoise_batch(fs, config, references=None, peak: float | None = None):
     refs = None
     if references is not None:
         refs = references if isinstance(references, np.ndarray) else np.stack([r.data for r in references])
-    u, traces, sts, _ = _solve(stack, refs, cfg, pk)
+    u, traces, sts, _ = _solve(stack, refs, cfg, pk, devices)
     for b, st in enumerate(sts):
         if st == N.CMG_DIVERGED:
             raise SolverDivergence(f"image {b}: objective became non-finite")

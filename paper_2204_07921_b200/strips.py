@@ -133,7 +133,8 @@ class CudaStrip:
         self.dtype = np.float64 if cfg.dtype == "float64" else np.float32
         self.esz = np.dtype(self.dtype).itemsize
         self._ptr = {}
-        for i in range(5):
+        self._stream = None
+        for i in range(6):
             p = ctypes.c_void_p()
             self._check(N.lib().cmg_plan_buffer(self.plan.handle, i, ctypes.byref(p)))
             self._ptr[i] = p.value
@@ -155,15 +156,42 @@ class CudaStrip:
         self._check(N.lib().cmg_buffer_download(self.plan.handle, index, N.ptr(a)))
         return a
 
+    # ---- asynchronous strip protocol: everything is enqueued on the plan's
+    # stream; the host synchronises once per V-cycle (read_partials) ----
+    def stream(self):
+        """torch view of the plan's CUDA stream (exchanges are issued on it)."""
+        import torch
+
+        if self._stream is None:
+            p = ctypes.c_void_p()
+            self._check(N.lib().cmg_plan_stream(self.plan.handle, ctypes.byref(p)))
+            self._stream = torch.cuda.ExternalStream(p.value, device=f"cuda:{self.plan.device}")
+        return self._stream
+
+    def begin(self):
+        self._check(N.lib().cmg_strip_begin(self.plan.handle, self.cfg.alpha, self.cfg.inner_iters))
+
     def level_step(self, layer: int, cur: int, out: int):
-        self._check(N.lib().cmg_level_step(self.plan.handle, layer, cur, out, self.cfg.alpha, self.cfg.inner_iters))
+        self._check(N.lib().cmg_level_step_async(self.plan.handle, layer, cur, out))
+
+    def energy_partials_async(self, cur: int, prev: int, use_ref: bool):
+        """Enqueue the owned rows' 5 energy sums + the non-finite flag into
+        device buffer 5; returns a torch tensor aliasing those 6 doubles."""
+        import torch
+
+        g = self.geom
+        self._check(N.lib().cmg_strip_partials_async(self.plan.handle, cur, prev, int(use_ref), g.local(g.g0),
+                                                     g.local(g.g1)))
+        return torch.as_tensor(_DevView(self._ptr[5], (6,), "<f8"), device=f"cuda:{self.plan.device}")
+
+    def read_partials(self) -> np.ndarray:
+        out = np.zeros(6)
+        self._check(N.lib().cmg_strip_read(self.plan.handle, N.dptr(out)))
+        return out
 
     def energy_partials(self, cur: int, prev: int, use_ref: bool) -> np.ndarray:
-        out = np.zeros(5)
-        g = self.geom
-        self._check(N.lib().cmg_energy_partials(self.plan.handle, cur, prev, int(use_ref), g.local(g.g0),
-                                                g.local(g.g1), N.dptr(out)))
-        return out
+        self.energy_partials_async(cur, prev, use_ref)
+        return self.read_partials()[:5]
 
     def rows(self, index: int, g_lo: int, g_hi: int):
         """torch CUDA tensor aliasing global rows [g_lo, g_hi) of buffer ``index``."""
@@ -175,10 +203,9 @@ class CudaStrip:
         v = _DevView(self._ptr[index] + off, (g_hi - g_lo, g.n), typestr)
         return torch.as_tensor(v, device=f"cuda:{self.plan.device}")
 
-    def sync(self):
-        import torch
-
-        torch.cuda.synchronize(self.plan.device)
+    def owned(self, index: int):
+        g = self.geom
+        return self.rows(index, g.g0, g.g1)
 
     def close(self):
         self.plan.close()
@@ -195,24 +222,39 @@ def _halo_pairs(geoms):
 
 
 class LocalExchange:
-    """All strips in this process (e.g. virtual strips on one GPU): copies."""
+    """All strips in this process (virtual strips, or one process driving
+    several GPUs): ghost rows are device-to-device copies issued on the
+    destination strip's stream, ordered against both strips' streams with
+    events; energy sums are added on the host (one read per strip per cycle)."""
 
     def __init__(self, strips):
         self.strips = strips
         self.pairs = _halo_pairs([s.geom for s in strips])
+        self.cuda = all(getattr(s, "is_cuda", False) for s in strips)
 
     def exchange(self, index: int):
-        for src, dst, lo, hi in self.pairs:
-            d = self.strips[dst].rows(index, lo, hi)
-            d.copy_(self.strips[src].rows(index, lo, hi))
-        # the copies run on torch's stream; libcmg's plan streams are
-        # non-blocking, so the next level step must not start before they land
-        for s in self.strips:
-            if hasattr(s, "sync"):
-                s.sync()
+        if not self.cuda:
+            for src, dst, lo, hi in self.pairs:
+                self.strips[dst].rows(index, lo, hi).copy_(self.strips[src].rows(index, lo, hi))
+            return
+        import torch
 
-    def allreduce(self, v: np.ndarray) -> np.ndarray:
-        return v
+        for src, dst, lo, hi in self.pairs:
+            ss, ds = self.strips[src].stream(), self.strips[dst].stream()
+            ready = torch.cuda.Event()
+            ready.record(ss)  # src rows final
+            ds.wait_event(ready)
+            with torch.cuda.stream(ds):
+                self.strips[dst].rows(index, lo, hi).copy_(self.strips[src].rows(index, lo, hi),
+                                                           non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(ds)  # src must not overwrite the rows before the copy ran
+            ss.wait_event(done)
+
+    def reduce_partials(self, tensors) -> np.ndarray:
+        if not self.cuda:
+            return np.sum([np.asarray(t) for t in tensors], axis=0)
+        return np.sum([s.read_partials() for s in self.strips], axis=0)
 
     def gather_owned(self, index: int):
         return [s.download(index)[s.geom.local(s.geom.g0):s.geom.local(s.geom.g1)] for s in self.strips]
@@ -220,7 +262,8 @@ class LocalExchange:
 
 class DistExchange:
     """One strip per rank; ghost rows and energy sums over torch.distributed
-    (NCCL for CUDA strips, gloo for CPU strips)."""
+    (NCCL for CUDA strips -- issued on the strip's plan stream, so nothing
+    waits on the host; gloo for CPU strips)."""
 
     def __init__(self, strip, geoms, rank: int, group=None):
         import torch.distributed as dist
@@ -231,6 +274,16 @@ class DistExchange:
         self.rank = rank
         self.group = group
         self.pairs = [p for p in _halo_pairs(geoms) if rank in (p[0], p[1])]
+        self.cuda = getattr(strip, "is_cuda", False)
+
+    def _on_stream(self):
+        import contextlib
+
+        if not self.cuda:
+            return contextlib.nullcontext()
+        import torch
+
+        return torch.cuda.stream(self.strip.stream())
 
     def exchange(self, index: int):
         dist = self.dist
@@ -238,26 +291,40 @@ class DistExchange:
         for src, dst, lo, hi in self.pairs:
             t = self.strip.rows(index, lo, hi)
             if src == self.rank:
-                ops.append(dist.P2POp(dist.isend, t.contiguous(), dst, self.group))
+                ops.append(dist.P2POp(dist.isend, t, dst, self.group))
             else:
                 ops.append(dist.P2POp(dist.irecv, t, src, self.group))
         if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
-        if hasattr(self.strip, "sync"):
-            self.strip.sync()
+            with self._on_stream():
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()  # NCCL: the plan stream waits, not the host
 
-    def allreduce(self, v: np.ndarray) -> np.ndarray:
-        import torch
-
-        dev = "cuda" if getattr(self.strip, "is_cuda", True) and torch.cuda.is_available() else "cpu"
-        t = torch.tensor(v, dtype=torch.float64, device=dev)
-        self.dist.all_reduce(t, group=self.group)
-        return t.cpu().numpy()
+    def reduce_partials(self, tensors) -> np.ndarray:
+        (t,) = tensors
+        with self._on_stream():
+            self.dist.all_reduce(t, group=self.group)
+        if self.cuda:
+            return self.strip.read_partials()  # the one host synchronisation of the cycle
+        return np.asarray(t, dtype=np.float64).copy()
 
     def gather_owned(self, index: int):
+        """Owned rows of every rank (tensor all-gather, rows padded to the
+        longest strip), on every rank."""
+        import torch
+
         s = self.strip
-        return [s.download(index)[s.geom.local(s.geom.g0):s.geom.local(s.geom.g1)]]
+        ws = len(self.geoms)
+        hmax = max(g.g1 - g.g0 for g in self.geoms)
+        own = s.owned(index) if self.cuda else torch.from_numpy(
+            np.ascontiguousarray(s.download(index)[s.geom.local(s.geom.g0):s.geom.local(s.geom.g1)]))
+        buf = torch.zeros((hmax, s.geom.n), dtype=own.dtype, device=own.device)
+        buf[: own.shape[0]].copy_(own)
+        outs = [torch.empty_like(buf) for _ in range(ws)]
+        with self._on_stream():
+            self.dist.all_gather(outs, buf, group=self.group)
+        if self.cuda:
+            s.stream().synchronize()
+        return [o[: g.g1 - g.g0].cpu().numpy() for o, g in zip(outs, self.geoms)]
 
 
 def _layer_sequence(cfg: SolverConfig):
@@ -268,16 +335,22 @@ def _layer_sequence(cfg: SolverConfig):
 
 
 def solve_strips(strips, exch, cfg: SolverConfig, npix: int, has_ref: bool = False, peak: float = 1.0):
-    """driver.denoise (driver.py:261-314) over strips; returns (final buffer index, trace)."""
+    """driver.denoise (driver.py:261-314) over strips; returns (final buffer index, trace).
+
+    Per V-cycle the host only enqueues (level steps, ghost-row exchanges,
+    energy sums and their all-reduce, all ordered on the strips' streams) and
+    synchronises once, to read the 5 energy sums + the non-finite flag."""
     import time
 
     t0 = time.perf_counter()
+    for s in strips:
+        s.begin()
 
     def partials(cur, prev):
-        v = np.zeros(5)
-        for s in strips:
-            v += s.energy_partials(cur, prev, has_ref)
-        return exch.allreduce(v)
+        v = exch.reduce_partials([s.energy_partials_async(cur, prev, has_ref) for s in strips])
+        if v[5] != 0.0:  # a non-finite correction during the cycle (hierarchy.py:122-123)
+            raise ValueError("corrections must be finite")
+        return v[:5]
 
     def energy_of(v):
         return float(v[0]) + (0.5 * cfg.alpha) * float(v[1])
@@ -376,8 +449,6 @@ def denoise_strips(f, config, parts: int = 2, reference=None, group=None):
         s.upload(4, ref[g.w0:g.w1])
     ex = DistExchange(s, geoms, rank, group)
     cur, tr = solve_strips([s], ex, cfg, m * n, ref is not None, peak)
-    own = s.download(cur)[g.local(g.g0):g.local(g.g1)].astype(np.float64)
-    parts_ = [None] * ws
-    dist.all_gather_object(parts_, own, group=group)
+    parts_ = ex.gather_owned(cur)
     s.close()
-    return Image(np.concatenate(parts_), peak), tr
+    return Image(np.concatenate(parts_).astype(np.float64), peak), tr

@@ -221,3 +221,18 @@ def test_nonfinite_energy_raises_solver_divergence():
         out = cmg.denoise_batch([cmg.Image(f, 1.0), cmg.Image(np.full((32, 32), 0.5), 1.0)],
                                 cmg.SolverConfig(max_outer=3))
     assert out is None
+
+
+def test_batch_sharded_over_devices_equals_one_plan():
+    """denoise_batch(devices=[...]) (cmg_mplan: contiguous image slices, one
+    host thread per shard) == one plan, bit for bit.  One GPU here: the same
+    device id twice gives two independent plans/streams on it."""
+    imgs = [synth.config_input(4, i)[0][:160, :144] for i in range(5)]
+    cfg = cmg.SolverConfig(mode="mean", layers=3, max_outer=8, epsilon=1e-5)
+    one = cmg.denoise_batch([cmg.Image(x, 1.0) for x in imgs], cfg)
+    two = cmg.denoise_batch([cmg.Image(x, 1.0) for x in imgs], cfg, devices=[0, 0])
+    three = cmg.denoise_batch([cmg.Image(x, 1.0) for x in imgs], cfg, devices=[0, 0, 0])
+    for (u1, t1), (u2, t2), (u3, t3) in zip(one, two, three):
+        assert np.array_equal(u1.data, u2.data) and np.array_equal(u1.data, u3.data)
+        assert t1.iterations == t2.iterations == t3.iterations
+        assert np.array_equal(t1.energies(), t2.energies()) and np.array_equal(t1.energies(), t3.energies())

@@ -44,6 +44,16 @@ class OracleStrip:
             out[4] = ((u[lo:hi] - self.buf[4][lo:hi]) ** 2).sum()
         return out
 
+    # asynchronous protocol (strips.solve_strips): begin / partials tensor with the
+    # non-finite flag appended
+    def begin(self):
+        pass
+
+    def energy_partials_async(self, cur, prev, use_ref):
+        import torch
+
+        return torch.from_numpy(np.append(self.energy_partials(cur, prev, use_ref), 0.0))
+
     def rows(self, index, g_lo, g_hi):
         import torch
 
@@ -115,9 +125,7 @@ def _worker(rank, ws, port, m, n, mode, q):
         st = OracleStrip(geoms[rank], cfg, f, clean)
         ex = S.DistExchange(st, geoms, rank)
         cur, tr = S.solve_strips([st], ex, cfg, m * n, True, 1.0)
-        own = ex.gather_owned(cur)[0]
-        parts = [None] * ws
-        dist.all_gather_object(parts, own)
+        parts = ex.gather_owned(cur)  # tensor all-gather of every rank's owned rows
         if rank == 0:
             q.put((np.concatenate(parts), tr.energies(), tr.iterations, tr.converged))
     finally:
