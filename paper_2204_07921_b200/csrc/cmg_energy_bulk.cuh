@@ -172,29 +172,29 @@ __global__ void __launch_bounds__(288) k_energy_bulk(EnergyArgs a, EnergyFin fz,
 #pragma unroll
                             for (int j = 0; j < PX; ++j) rv[j] = T(0);
                         }
-                        // per-pixel terms accumulate in fp64 (fp32 images: the curvature
-                        // term is evaluated in fp32, the fidelity / rel_u / PSNR terms from
-                        // exact fp64 differences of the fp32 values)
-                        double tv[NSUM][PX];
+                        // the PX (<= 4) terms of a thread's row segment are added in the image
+                        // precision, then accumulated in fp64: for fp32 a 4-term group adds at
+                        // most ~3 ulp of relative error, the size of the fp32 per-pixel terms
+                        // themselves (the per-row / 8-row chunks of k_energy are fp64 per pixel)
+                        A tv[NSUM][PX];
 #pragma unroll
                         for (int j = 0; j < PX; ++j) {
                             const A cc = C[j + 1];
-                            tv[0][j] = (double)curv_term<A>(cc, C[j + 2], C[j], N[j + 1], S[j + 1], N[j + 2], S[j],
-                                                            N[j], S[j + 2], a.mode);
-                            const double c64 = (double)cc;
-                            const double d = c64 - (double)fv[j];
+                            tv[0][j] = curv_term<A>(cc, C[j + 2], C[j], N[j + 1], S[j + 1], N[j + 2], S[j], N[j],
+                                                    S[j + 2], a.mode);
+                            const A d = cc - fv[j];
                             tv[1][j] = d * d;
-                            tv[2][j] = fabs(c64 - (double)pv[j]);
-                            tv[3][j] = fabs(c64);
-                            const double dr = c64 - (double)rv[j];
+                            tv[2][j] = fabs(cc - pv[j]);
+                            tv[3][j] = fabs(cc);
+                            const A dr = cc - rv[j];
                             tv[4][j] = dr * dr;
                         }
 #pragma unroll
                         for (int s = 0; s < NSUM; ++s) {
-                            double v = tv[s][0];
+                            A v = tv[s][0];
                             if (PX == 2) v = tv[s][0] + tv[s][1];
                             if (PX == 4) v = (tv[s][0] + tv[s][1]) + (tv[s][2] + tv[s][3]);
-                            acc[s] += v;
+                            acc[s] += (double)v;
                         }
                     }
 #pragma unroll
