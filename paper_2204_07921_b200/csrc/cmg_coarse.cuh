@@ -178,7 +178,7 @@ __device__ __forceinline__ T coarse_solve_thread(const Acc& U, const Acc& F, con
 #pragma unroll
             for (int l = 1; l < NPL; ++l) sum = O::add(sum, d[l]);
         }
-        chalf = O::div(sum, T(NPL));
+        chalf = div_pow2<T, NPL>(sum);  // NPL = 2^(J+2)
     } else {
         T v[NPL];
         static_for<0, NPL>([&](auto l) { plane_exact<T, decltype(l)::value>(U, ci, cc, uo, nullptr, &v[decltype(l)::value]); });
@@ -303,7 +303,7 @@ __device__ __forceinline__ T coarse_solve_team(const T* su, const T* sf, int bas
 #pragma unroll
                 for (int l = 1; l < NPL; ++l) sum = O::add(sum, __shfl_sync(FULL, d[l / TS], l % TS, TS));
             }
-            chalf = O::div(sum, T(NPL));
+            chalf = div_pow2<T, NPL>(sum);  // NPL = 2^(J+2)
         } else {
             ArgBest<T> bmin, bmax;
 #pragma unroll

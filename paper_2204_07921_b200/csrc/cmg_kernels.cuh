@@ -180,7 +180,7 @@ __device__ __forceinline__ T patch_solve_ct(const Acc& U, const Acc& F, int R0, 
 #pragma unroll
                 for (int l = 1; l < NPL; ++l) sum = O::add(sum, d[l]);
             }
-            chalf = O::div(sum, T(NPL));
+            chalf = div_pow2<T, NPL>(sum);  // NPL = 2^(J+2)
         }
     } else {
         T v[NPL];
@@ -429,7 +429,7 @@ __device__ __forceinline__ T patch_solve_team(const Acc& U, const AccF& F, int R
 #pragma unroll
             for (int l = 1; l < NPL; ++l) sum = O::add(sum, __shfl_sync(FULL, d[l / TS], l % TS, TS));
         }
-        chalf = O::div(sum, T(NPL));
+        chalf = div_pow2<T, NPL>(sum);  // NPL = 2^(J+2)
     } else {
         constexpr int PPL = NPL / TS;
         ArgBest<T> bmin, bmax;
@@ -552,7 +552,7 @@ __device__ __forceinline__ void bpp_body(const Acc& U, const Acc& F, int R0, int
                 sum = sh_vals[0];
                 for (int l = 1; l < NPL; ++l) sum = O::add(sum, sh_vals[l]);
             }
-            chalf = O::div(sum, T(NPL));
+            chalf = O::mul(sum, T(1.0 / NPL));  // NPL = 2^(J+2): exact reciprocal, same as the division
         } else {
             int imin = 0, imax = 0;
             if (!isnan(sh_vals[0])) {

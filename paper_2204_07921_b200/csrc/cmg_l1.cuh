@@ -124,7 +124,7 @@ __device__ __forceinline__ T l1_correction(const QuadAcc<T, TH, TW, P, Q>& A, T 
 #pragma unroll
                 for (int l = 1; l < 8; ++l) sum = O::add(sum, d[l]);
             }
-            chalf = O::div(sum, T(8));
+            chalf = div_pow2<T, 8>(sum);
         } else {
             T v[8];
             static_for<0, 8>([&](auto l) { plane_exact<T, decltype(l)::value>(acc, 0, 0, c, nullptr, &v[decltype(l)::value]); });
