@@ -50,6 +50,7 @@ typedef struct cmg_plan cmg_plan;
 int cmg_version(void);
 
 typedef struct cmg_mplan cmg_mplan;
+typedef struct cmg_radon cmg_radon;
 
 /* message of the last error on this thread ("" if none) */
 const char* cmg_last_error(void);
@@ -203,6 +204,29 @@ int cmg_host_free(void* p);
  * after one warm-up pass; *gbs = bytes * reps / elapsed (CUDA events).
  */
 int cmg_l2_read_bandwidth(int device, long long bytes, int reps, double* gbs);
+
+/*
+ * Curvature-regularised reconstruction (curvemg.reconstruction, fp64, device
+ * pointers, work enqueued on `stream`; paper_2204_07921_b200.recon drives
+ * them).  Parallel-beam Radon operator (reconstruction.py:123-183): the
+ * caller passes each pixel's lower detector bin i0 and upper-bin weight w
+ * per angle (n_angles x m*n, computed as the reference does); forward and
+ * adjoint are bit-identical to the reference's bincount / gather.
+ */
+int cmg_radon_create(cmg_radon** out, int m, int n, int n_angles, int detector_count, double pixel_size,
+                     const int* i0, const double* w, int device);
+int cmg_radon_destroy(cmg_radon* radon);
+int cmg_radon_forward(cmg_radon* radon, const double* x_dev, double* sino_dev, void* stream);
+int cmg_radon_adjoint(cmg_radon* radon, const double* y_dev, double* x_dev, void* stream);
+/* mean perpendicular plane distance at the patch centres of colour (p,q) of
+ * level `layer` (reconstruction.py:403-404; hc*wc outputs, row-major) */
+int cmg_recon_chalf(const double* u_dev, int m, int n, int layer, int p, int q, double* d_dev, void* stream);
+/* u += prolongation of the colour's corrections c (reconstruction.py:410-413, :432) */
+int cmg_recon_prolong(double* u_dev, const double* c_dev, int m, int n, int layer, int p, int q, void* stream);
+/* per-patch sums of img over the colour's patches (reconstruction.py:415-419) */
+int cmg_recon_block_sums(const double* img_dev, int m, int n, int layer, int p, int q, double* out_dev, void* stream);
+/* level-1 mean-curvature mass, nblocks partial sums (tangent.curvature_field) */
+int cmg_recon_curvature_partials(const double* u_dev, int m, int n, double* partial_dev, int nblocks, void* stream);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,8 @@ SYMBOLS = (
     "cmg_level_step", "cmg_energy_partials", "cmg_ssim_batch", "cmg_plan_ssim", "cmg_l2_read_bandwidth",
     "cmg_plan_stream", "cmg_strip_begin", "cmg_level_step_async", "cmg_strip_partials_async", "cmg_strip_read",
     "cmg_mplan_create", "cmg_mplan_destroy", "cmg_mplan_solve",
+    "cmg_radon_create", "cmg_radon_destroy", "cmg_radon_forward", "cmg_radon_adjoint", "cmg_recon_chalf",
+    "cmg_recon_prolong", "cmg_recon_block_sums", "cmg_recon_curvature_partials",
 )
 
 
@@ -71,6 +73,21 @@ def _declare(L):
     L.cmg_time_sweep.argtypes = [_vp, _i, _i, _i, _dp]
     L.cmg_host_alloc.restype = _vp
     L.cmg_host_alloc.argtypes = [ctypes.c_ulonglong]
+    L.cmg_radon_create.restype = _i
+    L.cmg_radon_create.argtypes = [ctypes.POINTER(_vp), _i, _i, _i, _i, _d, _ip, _dp, _i]
+    L.cmg_radon_destroy.restype = _i
+    L.cmg_radon_destroy.argtypes = [_vp]
+    for nm in ("cmg_radon_forward", "cmg_radon_adjoint"):
+        getattr(L, nm).restype = _i
+        getattr(L, nm).argtypes = [_vp, _vp, _vp, _vp]
+    L.cmg_recon_chalf.restype = _i
+    L.cmg_recon_chalf.argtypes = [_vp, _i, _i, _i, _i, _i, _vp, _vp]
+    L.cmg_recon_prolong.restype = _i
+    L.cmg_recon_prolong.argtypes = [_vp, _vp, _i, _i, _i, _i, _i, _vp]
+    L.cmg_recon_block_sums.restype = _i
+    L.cmg_recon_block_sums.argtypes = [_vp, _i, _i, _i, _i, _i, _vp, _vp]
+    L.cmg_recon_curvature_partials.restype = _i
+    L.cmg_recon_curvature_partials.argtypes = [_vp, _i, _i, _vp, _i, _vp]
     L.cmg_mplan_create.restype = _i
     L.cmg_mplan_create.argtypes = [ctypes.POINTER(_vp), _i, _i, _i, _i, _i, _i, _i, _ip, _i]
     L.cmg_mplan_destroy.restype = _i

@@ -50,6 +50,12 @@ inline bool single_chunk(int len, int pad_after) { return len >= 2 && pad_after 
 }  // namespace
 
 namespace cmg {
+// error reporting for the other translation units (cmg_recon.cu)
+int set_error(int code, const char* msg) {
+    g_err = msg;
+    return code;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
