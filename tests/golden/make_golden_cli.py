@@ -26,6 +26,8 @@ CASES = {
                                "--mode", "gaussian", "--stop", "u", "--epsilon", "1e-3", "--layers", "4",
                                "--max-outer", "30", "--threads", "1", "--clip"],
     "bench_sizes": ["bench", "--sizes", "64,96", "--bench-iters", "4", "--threads", "1"],
+    "mri_radial": ["mri", "--phantom", "shepp_logan", "--size", "48", "--sigma", "4", "--rate", "0.3",
+                   "--layers", "2", "--max-outer", "4", "--epsilon", "1e-300", "--threads", "1"],
 }
 
 

@@ -14,7 +14,7 @@ from paper_2204_07921_b200 import cli
 from paper_2204_07921_b200.phantoms import phantom
 
 GOLD = Path(__file__).resolve().parent / "golden" / "cli"
-CASES = ["denoise_triangle", "denoise_shepp_gc_rel_u", "bench_sizes"]
+CASES = ["denoise_triangle", "denoise_shepp_gc_rel_u", "bench_sizes", "mri_radial"]
 
 # the reference CLI invocations (make_golden_cli.CASES)
 ARGS = {
@@ -24,6 +24,8 @@ ARGS = {
                                "--mode", "gaussian", "--stop", "u", "--epsilon", "1e-3", "--layers", "4",
                                "--max-outer", "30", "--threads", "1", "--clip"],
     "bench_sizes": ["bench", "--sizes", "64,96", "--bench-iters", "4", "--threads", "1"],
+    "mri_radial": ["mri", "--phantom", "shepp_logan", "--size", "48", "--sigma", "4", "--rate", "0.3",
+                   "--layers", "2", "--max-outer", "4", "--epsilon", "1e-300", "--threads", "1"],
 }
 
 
@@ -84,32 +86,51 @@ def test_cli_outputs_match_reference(case, tmp_path):
         for a, b in zip(ours[2:], ref[2:]):
             assert a[:3] == b[:3]  # size, pixels, iterations (seconds / ratios are timings)
         return
-    # images: byte-identical files (fp64 exact path is bit-identical to the reference)
-    for f in sorted(p.name for p in g.iterdir() if p.name.startswith(("noisy", "restored"))):
-        assert (tmp_path / f).read_bytes() == (g / f).read_bytes(), f
+    recon = case.startswith("mri")
+    if recon:  # reconstruction: inner products / FFT sum in another order -> rounding-level agreement
+        assert (tmp_path / "mask.pgm").read_bytes() == (g / "mask.pgm").read_bytes()
+        for f in ("kspace.csv", "restored.csv"):
+            a, b = np.loadtxt(tmp_path / f, delimiter=","), np.loadtxt(g / f, delimiter=",")
+            assert np.abs(a - b).max() <= 1e-7 * max(1.0, np.abs(b).max()), f
+    else:
+        # images: byte-identical files (fp64 exact path is bit-identical to the reference)
+        for f in sorted(p.name for p in g.iterdir() if p.name.startswith(("noisy", "restored"))):
+            assert (tmp_path / f).read_bytes() == (g / f).read_bytes(), f
     # trace: same rows; energies within the device-sum tolerance, seconds differ
     h1, r1 = _trace(tmp_path / "trace.csv")
     h2, r2 = _trace(g / "trace.csv")
     assert h1 == h2 and len(r1) == len(r2)
     for a, b in zip(r1, r2):
         assert a[0] == b[0]
-        assert abs(float(a[1]) - float(b[1])) <= 1e-12 * abs(float(b[1]))
+        assert abs(float(a[1]) - float(b[1])) <= (1e-8 if recon else 1e-12) * abs(float(b[1]))
         for k in (2, 3):  # rel_energy, rel_u (empty at iteration 0)
             assert (a[k] == "") == (b[k] == "")
             if b[k]:
-                assert abs(float(a[k]) - float(b[k])) <= 1e-9 * abs(float(b[k])) + 1e-12
-        assert abs(float(a[5]) - float(b[5])) <= 1e-9
+                tol = 1e-6 if recon else 1e-9
+                assert abs(float(a[k]) - float(b[k])) <= tol * abs(float(b[k])) + 1e-12
+        assert abs(float(a[5]) - float(b[5])) <= (1e-7 if recon else 1e-9)
     # report.json: identical except the wall time and the GPU energy sum order
     ro = json.loads((tmp_path / "report.json").read_text())
     rr = json.loads((g / "report.json").read_text())
-    for k in ("command", "converged", "iterations", "psnr", "ssim"):
+    for k in ("command", "converged", "iterations"):
         assert ro[k] == rr[k], k
-    assert abs(ro["energy"] - rr["energy"]) <= 1e-12 * abs(rr["energy"])
+    for k in ("psnr", "ssim"):
+        assert ro[k] == rr[k] if not recon else abs(ro[k] - rr[k]) <= 1e-7, k
+    assert abs(ro["energy"] - rr["energy"]) <= (1e-8 if recon else 1e-12) * abs(rr["energy"])
     ro["config"].pop("output_dir"), rr["config"].pop("output_dir")
     assert ro["config"] == rr["config"]
     assert set(ro) == set(rr)
 
 
-def test_cli_reconstruction_commands_exit_error(tmp_path, capsys):
-    assert cli.run(cli.manifest_from_args(["ct", "--output-dir", str(tmp_path)])) == cli.EXIT_ERROR
-    assert "not on the B200 backend" in capsys.readouterr().err
+@pytest.mark.gpu
+def test_cli_ct_runs_on_gpu(tmp_path):
+    """The reference's `ct` command raises TypeError (it passes value_range= to
+    reconstruct); here it runs the intended reconstruction."""
+    code = cli.run(cli.manifest_from_args(["ct", "--phantom", "shepp_logan", "--size", "48", "--projections", "16",
+                                           "--layers", "2", "--max-outer", "3", "--epsilon", "1e-300",
+                                           "--output-dir", str(tmp_path)]))
+    assert code == cli.EXIT_NOT_CONVERGED
+    rep = json.loads((tmp_path / "report.json").read_text())
+    assert rep["iterations"] == 3 and np.isfinite(rep["energy"]) and rep["psnr"] > 10
+    for f in ("sinogram.csv", "sinogram.csv.json", "restored.csv", "trace.csv", "manifest.json"):
+        assert (tmp_path / f).exists(), f
