@@ -461,7 +461,7 @@ int cmg_plan_destroy(cmg_plan* P) {
     cudaSetDevice(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     if (P->exec) cudaGraphExecDestroy(P->exec);
-    void* ptrs[] = {P->u, P->uprev, P->ubuf[2], P->f, P->ref, P->upad, P->epad, P->partials, P->st, P->ndone, P->eonly, P->raw5, P->P, P->stamps, P->tickets, P->fsum[2], P->fsum[3], P->rpsync};
+    void* ptrs[] = {P->u, P->uprev, P->ubuf[2], P->f, P->ref, P->upad, P->epad, P->partials, P->st, P->ndone, P->eonly, P->raw5, P->P, P->stamps, P->tickets, P->fsum[2], P->fsum[3]};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 5; ++i)
@@ -720,14 +720,6 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     if (const char* lw = getenv("CMG_L1_WIDE")) P->l1_wide = atoi(lw) != 0;
     if (const char* en = getenv("CMG_ENERGY_NT")) P->energy_nt = atoi(en) == 512 ? 512 : 256;
     CKP(cudaMalloc(&P->P, sizeof(SolveParams)));
-    {  // counters of the one-launch row-parity kernel (self-resetting)
-        long long rows = 0;
-        for (int j = 2; j <= std::min(layers, 3); ++j) rows = std::max<long long>(rows, (P->lv[j].mj + 1) / 2);
-        P->rpsync_rows = rows * batch;
-        if (const char* rb = getenv("CMG_RP_BOTH")) P->rp_both = atoi(rb);
-        CKP(cudaMalloc(&P->rpsync, sizeof(int) * (size_t)(2 + P->rpsync_rows)));
-        CKP(cudaMemset(P->rpsync, 0, sizeof(int) * (size_t)(2 + P->rpsync_rows)));
-    }
 #undef CKP
     *out = P;
     return CMG_OK;

@@ -403,25 +403,6 @@ void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
     const size_t smem = sizeof(T) * (G::ROWS + (fs ? 0 : G::S)) * G::WIN;
     auto kern = k_rowpair<T, LAYER, MODE, PREC, TS, NT>;
     smem_attr(kern, smem);
-    const int rows0 = (L.mj + 1) / 2, rows1 = L.mj / 2;
-    if (P->rp_both && P->rpsync && rows0 > 0 && rows1 > 0 && (long long)rows0 * P->B <= P->rpsync_rows) {
-        // both parities in one launch (k_rowpair_both)
-        RowPairArgs<T> r1 = r;
-        r.c0 = make_sweep_args<T>(P, LAYER, 0);
-        r.c1 = make_sweep_args<T>(P, LAYER, 1);
-        r1.c0 = make_sweep_args<T>(P, LAYER, 2);
-        r1.c1 = make_sweep_args<T>(P, LAYER, 3);
-        auto kb = k_rowpair_both<T, LAYER, MODE, PREC, TS, NT>;
-        smem_attr(kb, smem);
-        RPSync sy;
-        sy.next = P->rpsync;
-        sy.done = P->rpsync + 1;
-        sy.rowdone = P->rpsync + 2;
-        const int items = r.ntiles * (rows0 + rows1) * P->B;
-        klaunch(P, kb, dim3(items), G::NT, smem, r, r1, sy, rows0, rows1, P->B);
-        stamp(P, 10 * LAYER + 8);
-        return;
-    }
     for (int p = 0; p < 2; ++p) {
         const int rows = (L.mj - p + 1) / 2;
         if (rows <= 0) continue;

@@ -86,9 +86,6 @@ struct cmg_plan {
     int rowpair = 3;        // bit j-2: level j (2, 3) runs as two row-parity launches (k_rowpair)
     bool l1_wide = false;   // k_l1_tile with 32 x 64 tiles (CMG_L1_WIDE)
     int rp_ts2 = 4;         // lanes per patch of the level-2 row-parity kernel (CMG_RP_TS2)
-    int rp_both = 1;        // both row parities of a level in one launch (k_rowpair_both; CMG_RP_BOTH=0: two)
-    int* rpsync = nullptr;  // its counters: next, done, rowdone[rpsync_rows]
-    long long rpsync_rows = 0;
     int rp1 = 0;            // bit j-2: level j's row-parity kernel runs one thread per patch (CMG_RP1)
     int rp_bulk = 1;        // ... as the persistent bulk-copy kernel (CMG_RP_BULK)
     int rp_stages = 1;      // shared-memory stages of that kernel (CMG_RP_STAGES: 1 or 2; 1 = more CTAs per SM, faster)

@@ -274,77 +274,6 @@ __global__ void __launch_bounds__(NT) k_rowpair(RowPairArgs<T> a) {
 }
 
 // ---------------------------------------------------------------------------
-// Both row parities of a level in ONE launch.  CTAs take a logical item index
-// from an atomic counter in dispatch order: the parity-0 items first, then the
-// parity-1 items, and a parity-1 item waits (spinning on per-patch-row
-// completion counters) until the parity-0 patch rows above and below it are
-// written.  The dependency only points to items with a smaller logical index,
-// i.e. to CTAs already running, so it cannot deadlock.  The last CTA to finish
-// resets the counters for the next launch.
-// ---------------------------------------------------------------------------
-struct RPSync {
-    int* next;     // logical item counter
-    int* done;     // finished-CTA ticket
-    int* rowdone;  // [B][rows0] parity-0 tiles written per patch row
-};
-
-template <typename T, int LAYER, int MODE, int PREC, int TS, int NT = 256>
-__global__ void __launch_bounds__(NT) k_rowpair_both(RowPairArgs<T> a0, RowPairArgs<T> a1, RPSync sy, int rows0,
-                                                     int rows1, int B) {
-    pdl_sync();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* win = reinterpret_cast<T*>(smem_raw);
-    __shared__ int s_id, s_last;
-    const int nt = a0.ntiles;
-    const int total0 = nt * rows0 * B, total = total0 + nt * rows1 * B;
-    if (threadIdx.x == 0) s_id = atomicAdd(sy.next, 1);
-    __syncthreads();
-    const int id = s_id;
-    const int par = id >= total0 ? 1 : 0;
-    const int r = par ? id - total0 : id;
-    const int rows = par ? rows1 : rows0;
-    const int b = r / (nt * rows), rr = r - b * nt * rows;
-    const int pr = rr / nt, tile = rr - pr * nt;
-    auto body = [&](const RowPairArgs<T>& a) {
-        const RPItem<T> it = rp_item<T, LAYER, TS, NT>(a, b, pr, tile);
-        if (a.c0.st[b].done) return;
-        if (par == 1 && threadIdx.x == 0) {  // parity-0 patch rows 2pr and 2pr+2 written?
-            const volatile int* rd = sy.rowdone + (long long)b * rows0;
-            while (rd[pr] < nt) __nanosleep(64);
-            if (pr + 1 < rows0)
-                while (rd[pr + 1] < nt) __nanosleep(64);
-            __threadfence();
-        }
-        __syncthreads();
-        rp_stage<T, LAYER, TS, NT>(a, it, win);
-        __syncthreads();
-        rp_compute<T, LAYER, MODE, PREC, TS, NT>(a, it, win);
-        if (par == 0) {
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                __threadfence();
-                atomicAdd(sy.rowdone + (long long)b * rows0 + pr, 1);
-            }
-        }
-    };
-    if (par)
-        body(a1);
-    else
-        body(a0);
-    // the last CTA resets the counters for the next launch
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(sy.done, 1) == total - 1);
-    __syncthreads();
-    if (s_last) {
-        for (int i = threadIdx.x; i < rows0 * B; i += NT) sy.rowdone[i] = 0;
-        if (threadIdx.x == 0) {
-            *sy.next = 0;
-            *sy.done = 0;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Large jobs, fast mean mode with per-patch f sums: the same row-parity
 // launches, one thread per patch, as a PERSISTENT kernel whose windows are
 // streamed by bulk asynchronous copies (cp.async.bulk + mbarrier, one copy per
