@@ -187,10 +187,17 @@ __global__ void __launch_bounds__(288) k_energy_bulk(EnergyArgs a, EnergyFin fz,
                             tv[2][j] = fabs(cc - pv[j]);
                             tv[3][j] = fabs(cc);
                             const A dr = cc - rv[j];
-                            tv[4][j] = dr * dr;
+                            tv[4][j] = has_ref ? dr * dr : A(0);
                         }
 #pragma unroll
-                        for (int s = 0; s < NSUM; ++s) {
+                        for (int s = 0; s < NSUM - 1; ++s) {
+                            A v = tv[s][0];
+                            if (PX == 2) v = tv[s][0] + tv[s][1];
+                            if (PX == 4) v = (tv[s][0] + tv[s][1]) + (tv[s][2] + tv[s][3]);
+                            acc[s] += (double)v;
+                        }
+                        if (has_ref) {  // (u - ref)^2 only with a reference image
+                            constexpr int s = NSUM - 1;
                             A v = tv[s][0];
                             if (PX == 2) v = tv[s][0] + tv[s][1];
                             if (PX == 4) v = (tv[s][0] + tv[s][1]) + (tv[s][2] + tv[s][3]);

@@ -637,19 +637,41 @@ constexpr int NSUM = 5;  // curv, fid, |du|, |u|, (u-ref)^2
 
 // level-1 curvature term of one pixel from its 3x3 neighbourhood, in the
 // accumulation precision A (double for fp64 images, float for fp32 images;
-// the per-row sums are accumulated in double either way)
+// the sums are accumulated in double either way).  kappa_p = (u+p + u-p -
+// 2 u) / (2 |p|^2) is evaluated as fma(u+p + u-p, 1/(2|p|^2), -u/|p|^2):
+// the scalings are powers of two, so this is the same correctly rounded value
+// with one instruction less.  A NaN anywhere makes the term NaN (np.min /
+// np.max propagate NaN); for fp32 the NaN-propagating min/max instructions do
+// that, for fp64 an explicit test.
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+    float d;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float d;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+
 template <typename A>
 __device__ __forceinline__ A curv_term(A uo, A uE, A uW, A uN, A uS, A uNE, A uSW, A uNW, A uSE, int mode) {
-    const A two = A(2) * uo;
-    const A k0 = ((uE + uW) - two) * A(0.5);
-    const A k1 = ((uN + uS) - two) * A(0.5);
-    const A k2 = ((uNE + uSW) - two) * A(0.25);
-    const A k3 = ((uNW + uSE) - two) * A(0.25);
-    const A kmin = fmin(fmin(k0, k1), fmin(k2, k3));
-    const A kmax = fmax(fmax(k0, k1), fmax(k2, k3));
-    A term = (mode == MODE_MEAN) ? fabs(A(0.5) * (kmin + kmax)) : fabs(kmin * kmax);
-    if (isnan(k0) || isnan(k1) || isnan(k2) || isnan(k3)) term = A(NAN);
-    return term;
+    const A h = A(-0.5) * uo;
+    const A k0 = fma(uE + uW, A(0.5), -uo);
+    const A k1 = fma(uN + uS, A(0.5), -uo);
+    const A k2 = fma(uNE + uSW, A(0.25), h);
+    const A k3 = fma(uNW + uSE, A(0.25), h);
+    if constexpr (sizeof(A) == 4) {
+        const float kmin = fmin_nan(fmin_nan(k0, k1), fmin_nan(k2, k3));
+        const float kmax = fmax_nan(fmax_nan(k0, k1), fmax_nan(k2, k3));
+        return (mode == MODE_MEAN) ? fabsf(0.5f * (kmin + kmax)) : fabsf(kmin * kmax);
+    } else {
+        const A kmin = fmin(fmin(k0, k1), fmin(k2, k3));
+        const A kmax = fmax(fmax(k0, k1), fmax(k2, k3));
+        A term = (mode == MODE_MEAN) ? fabs(A(0.5) * (kmin + kmax)) : fabs(kmin * kmax);
+        if (isnan(k0) || isnan(k1) || isnan(k2) || isnan(k3)) term = A(NAN);
+        return term;
+    }
 }
 
 struct TraceArgs {
