@@ -213,10 +213,14 @@ __device__ __forceinline__ void l1_energy_sums(const T* su, const T* sf, int R, 
     constexpr int PH = TH / 2, PW = TW / 2, CNT = PH * PW;
     static_assert(G::HALO % 2 == 0, "owned pixels start on an even region row");
     double acc[NSUM] = {0, 0, 0, 0, 0};
+    // fully unrolled (2 pixels per plane and thread for 32 x 64 tiles): the u_prev
+    // loads of all of a thread's pixels are issued before the first use
     static_for<0, 4>([&](auto cp) {
         constexpr int P = decltype(cp)::value >> 1, Q = decltype(cp)::value & 1;
-#pragma unroll 1
-        for (int t = threadIdx.x; t < CNT; t += blockDim.x) {
+#pragma unroll
+        for (int it = 0; it < (CNT + 255) / 256; ++it) {
+            const int t = threadIdx.x + it * 256;
+            if (CNT % 256 != 0 && t >= CNT) continue;
             const int ii = t / PW, kk = t % PW;
             const int gi = R + 2 * ii + P, gk = C + 2 * kk + Q;
             if (gi >= m || gk >= n) continue;
