@@ -112,7 +112,9 @@ __device__ __forceinline__ F2 l1_chalf_x2(F2 c, F2 E, F2 W, F2 N, F2 S, F2 NE, F
     return mul2(fma2(f2_splat(1.41421356237309505f), t3 + t4, t1 + t2), f2_splat(0.125f), nz);
 }
 
-template <int TH, int TW, int NR, bool FAST = true, int NT = 256>
+// FG: f is not staged in shared memory but read from global memory (L2) by
+// the pixel's own phase: half the shared memory per CTA, more CTAs per SM
+template <int TH, int TW, int NR, bool FAST = true, int NT = 256, bool FG = false>
 __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     pdl_sync();
     using G = L1Geom<float, TH, TW>;
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
         for (int j = 0; j < NV4; ++j) {
             if (G::RH % RSTEP == 0 || row + j * RSTEP < G::RH) {
                 uv[j] = __ldg(ub + j * rstride4);
-                fv4[j] = __ldg(fbp + j * rstride4);
+                if constexpr (!FG) fv4[j] = __ldg(fbp + j * rstride4);
             }
         }
         const int s0 = (row & 1) * 2 * G::PLANE + (row >> 1) * G::QW + 2 * c4;  // plane (p,0), word 2*c4
@@ -173,8 +175,10 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
                 const int o = s0 + j * (RSTEP / 2) * G::QW;
                 *reinterpret_cast<unsigned long long*>(su + o) = f2_pack(uv[j].x, uv[j].z).v;
                 *reinterpret_cast<unsigned long long*>(su + o + G::PLANE) = f2_pack(uv[j].y, uv[j].w).v;
-                *reinterpret_cast<unsigned long long*>(sf + o) = f2_pack(fv4[j].x, fv4[j].z).v;
-                *reinterpret_cast<unsigned long long*>(sf + o + G::PLANE) = f2_pack(fv4[j].y, fv4[j].w).v;
+                if constexpr (!FG) {
+                    *reinterpret_cast<unsigned long long*>(sf + o) = f2_pack(fv4[j].x, fv4[j].z).v;
+                    *reinterpret_cast<unsigned long long*>(sf + o + G::PLANE) = f2_pack(fv4[j].y, fv4[j].w).v;
+                }
             }
         }
     } else {
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
             if (gi >= 0 && gi < m && gk >= 0 && gk < n) {
                 const long long g = (long long)gi * n + gk;
                 su[G::idx(i, k)] = uin[g];
-                sf[G::idx(i, k)] = f[g];
+                if constexpr (!FG) sf[G::idx(i, k)] = f[g];
             }
         }
     }
@@ -243,7 +247,13 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
                     using ICEW = std::integral_constant<int, PL_ew>;
                     using ICD = std::integral_constant<int, PL_d>;
                     const F2 cv = lds2(sb + (PL_c + OFF));
-                    const F2 fv = lds2(fb + (PL_c + OFF));
+                    F2 fv;
+                    if constexpr (FG) {  // pixels (i, 4pj+Q) and (i, 4pj+Q+2) of the region
+                        const float* fp = f + (long long)(r0 + 2 * qi + P) * n + c0 + 4 * pj + Q;
+                        fv = f2_pack(__ldg(fp), __ldg(fp + 2));
+                    } else {
+                        fv = lds2(fb + (PL_c + OFF));
+                    }
                     const F2 Nv = lds2(sb + (PL_ns + OFF + aN * G::QW));
                     const F2 Sv = lds2(sb + (PL_ns + OFF + aS * G::QW));
                     F2 Ev, Wv, NEv, NWv, SEv, SWv;
@@ -300,7 +310,14 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
                 }
             };
             const F2 cv = lds2(su + PL_c + base);
-            const F2 fv = lds2(sf + PL_c + base);
+            F2 fv;
+            if constexpr (FG) {  // clamped: out-of-image pixels are discarded below
+                const int gi = min(max(r0 + 2 * qi + P, 0), m - 1);
+                const int ga = min(max(c0 + 4 * pj + Q, 0), n - 1), gb = min(max(c0 + 4 * pj + Q + 2, 0), n - 1);
+                fv = f2_pack(__ldg(f + (long long)gi * n + ga), __ldg(f + (long long)gi * n + gb));
+            } else {
+                fv = lds2(sf + PL_c + base);
+            }
             const F2 Nv = lds2(su + PL_ns + base + aN * G::QW);
             const F2 Sv = lds2(su + PL_ns + base + aS * G::QW);
             F2 Ev, Wv, NEv, NWv, SEv, SWv;

@@ -285,7 +285,7 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
             auto go = [&](auto kern, auto th, auto tw, int nt) {
                 constexpr int TH = decltype(th)::value, TW = decltype(tw)::value;
                 using G = L1Geom<float, TH, TW>;
-                const size_t smem = sizeof(float) * (2 + 8 * G::PLANE);
+                const size_t smem = sizeof(float) * (2 + (P->l1x2 >= 11 ? 4 : 8) * G::PLANE);
                 smem_attr(kern, smem);
                 const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
                 klaunch(P, kern, grd, nt, smem, a);
@@ -303,6 +303,8 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
                 case 6: go(k_l1_x2<56, 120, 0, false>, I56{}, I120{}, 256); break;
                 case 7: go(k_l1_x2<56, 120, 0, true, 512>, I56{}, I120{}, 512); break;
                 case 8: go(k_l1_x2<120, 56, 0>, I120{}, I56{}, 256); break;
+                case 11: go(k_l1_x2<56, 120, 0, true, 256, true>, I56{}, I120{}, 256); break;
+                case 12: go(k_l1_x2<56, 56, 0, true, 256, true>, I56{}, I56{}, 256); break;
                 default: go(k_l1_x2<56, 56, 0>, I56{}, I56{}, 256); break;
             }
             return;
