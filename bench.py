@@ -517,7 +517,8 @@ def l1_kernel_name(dtype: str, prec: str, m: int, n: int) -> str:
     """The level-1 kernel the plan dispatches (cmg.cu plan heuristics)."""
     if dtype == "float32" and prec == "fast":
         tile = "56, 120" if m * n >= (4 << 20) and n >= 240 else "56, 56"
-        return f"k_l1_x2<{tile}> (level-1 sweep, four colours in one launch, packed f32x2)"
+        fsrc = ", f from L2" if tile == "56, 120" else ""
+        return f"k_l1_x2<{tile}{fsrc}> (level-1 sweep, four colours in one launch, packed f32x2)"
     t = "double" if dtype == "float64" else "float"
     return f"k_l1_tile<{t}, {prec}> (level-1 sweep, four colours in one launch)"
 

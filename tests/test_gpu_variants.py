@@ -116,6 +116,8 @@ VARIANTS32_EXACT = {
     "l1_tiles_56x120": {"CMG_L1X2": "4"},
     "l1_tiles_120x56": {"CMG_L1X2": "8"},
     "l1_tiles_88x88_192_threads": {"CMG_L1X2": "5"},
+    "l1_f_from_global_56x120": {"CMG_L1X2": "11"},
+    "l1_f_from_global_56x56": {"CMG_L1X2": "12"},
     "energy_bulk_copies": {"CMG_EBULK": "1"},
     "host_chunked_graph": {"CMG_NO_WHILE": "1"},
 }
