@@ -700,8 +700,7 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     // packed k_l1_x2 kernel and the separate bulk energy pass) sums the energy of its
     // input; partials per level-1 CTA (tiles >= 32 x 32)
     {
-        const bool x2 = dtype == CMG_F32 && P->prec == CMG_PREC_FAST && mode == CMG_MODE_MEAN && P->l1x2;
-        P->efuse = P->fused && P->fused_finalize && !x2;
+        P->efuse = P->fused && P->fused_finalize;
         if (const char* ef = getenv("CMG_EFUSE")) P->efuse = P->efuse && atoi(ef) != 0;
     }
     const long long l1tiles = (long long)((m + 31) / 32) * ((n + 31) / 32);

@@ -112,6 +112,48 @@ __device__ __forceinline__ F2 l1_chalf_x2(F2 c, F2 E, F2 W, F2 N, F2 S, F2 NE, F
     return mul2(fma2(f2_splat(1.41421356237309505f), t3 + t4, t1 + t2), f2_splat(0.125f), nz);
 }
 
+// Energy terms of the tile's owned pixels (energy-fused cycle, fp32 images):
+// as l1_energy_sums, with f from shared memory or (FG) global memory; each
+// thread adds its <= 7 pixels of a colour plane in fp32 (<= 6 ulp relative,
+// the size of the fp32 per-pixel terms) before the fp64 accumulators
+template <int TH, int TW, bool FG>
+__device__ __forceinline__ void x2_energy_sums(const float* su, const float* sf, const float* f, int R, int C,
+                                               int m, int n, const float* up, const float* rf, double* partials,
+                                               int b, int cta, int nbx) {
+    using G = L1Geom<float, TH, TW>;
+    constexpr int PH = TH / 2, PW = TW / 2, CNT = PH * PW;
+    double acc[NSUM] = {0, 0, 0, 0, 0};
+    static_for<0, 4>([&](auto cp) {
+        constexpr int P = decltype(cp)::value >> 1, Q = decltype(cp)::value & 1;
+        float loc[NSUM] = {0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+        for (int t = threadIdx.x; t < CNT; t += blockDim.x) {
+            const int ii = t / PW, kk = t % PW;
+            const int gi = R + 2 * ii + P, gk = C + 2 * kk + Q;
+            if (gi >= m || gk >= n) continue;
+            const QuadAcc<float, TH, TW, P, Q> A{su, G::HALO / 2 + ii, G::HALO / 2 + kk};
+            const float c = A.template at<0, 0>();
+            const long long g = (long long)gi * n + gk;
+            const float fv = FG ? __ldg(f + g)
+                                : sf[(P * 2 + Q) * G::PLANE + (G::HALO / 2 + ii) * G::QW + G::HALO / 2 + kk];
+            loc[0] += curv_term<float>(c, A.template at<0, 1>(), A.template at<0, -1>(), A.template at<-1, 0>(),
+                                       A.template at<1, 0>(), A.template at<-1, 1>(), A.template at<1, -1>(),
+                                       A.template at<-1, -1>(), A.template at<1, 1>(), MODE_MEAN);
+            const float d = c - fv;
+            loc[1] += d * d;
+            loc[2] += fabsf(c - __ldg(up + g));
+            loc[3] += fabsf(c);
+            if (rf) {
+                const float dr = c - __ldg(rf + g);
+                loc[4] += dr * dr;
+            }
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < NSUM; ++s2) acc[s2] += (double)loc[s2];
+    });
+    cta_sums_store(acc, partials, nbx, cta, b);
+}
+
 // FG: f is not staged in shared memory but read from global memory (L2) by
 // the pixel's own phase: half the shared memory per CTA, more CTAs per SM
 template <int TH, int TW, int NR, bool FAST = true, int NT = 256, bool FG = false>
@@ -131,7 +173,11 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     const float* f = a.f + (long long)b * a.istride;
     float* uout = a.uout + (long long)b * a.istride;
     const int m = a.m, n = a.n;
-    if (a.st[b].done) return;  // stopped image (final u in ImgState::final_buf)
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x, nbx = gridDim.x * gridDim.y;
+    if (a.st[b].done) {  // stopped image (final u in ImgState::final_buf)
+        if (a.efuse) efused_ticket(a.fz, a.partials, nbx, b, reinterpret_cast<double*>(smem_raw));
+        return;
+    }
     const int r0 = R - G::HALO, c0 = C - G::HALO;
     const bool border = (r0 < 1) || (c0 < 1) || (r0 + G::RH >= m) || (c0 + G::RW >= n);
     const bool vec = !border && (n % 4 == 0);
@@ -194,6 +240,9 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     }
     __syncthreads();
     if (border) l1_reflect_fix<float, TH, TW>(su, r0, c0, m, n);
+    if (a.efuse)
+        x2_energy_sums<TH, TW, FG>(su, sf, f, R, C, m, n, a.uprev + (long long)b * a.istride,
+                                   a.ref ? a.ref + (long long)b * a.istride : nullptr, a.partials, b, cta, nbx);
     const F2 w2 = f2_splat((float)a.P->w[1][0]);
     const F2 inv2 = f2_splat((float)(1.0 / a.P->den[1][0]));
     const F2 nz2 = f2_splat(a.nz);  // -0.0f (see mul2)
@@ -389,7 +438,16 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     float fa0, fa1;
     f2_unpack(finite_acc, fa0, fa1);
     const bool bad = !(isfinite(fa0) && isfinite(fa1));
-    if (__syncthreads_or(bad) && threadIdx.x == 0) a.st[b].bad = 1;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) {
+        if (a.efuse)
+            a.st[b].bad1 = 1;
+        else
+            a.st[b].bad = 1;
+    }
+    if (a.efuse) {
+        __syncthreads();  // shared memory becomes the finalize scratch
+        efused_ticket(a.fz, a.partials, nbx, b, reinterpret_cast<double*>(smem_raw));
+    }
 }
 
 }  // namespace cmg
