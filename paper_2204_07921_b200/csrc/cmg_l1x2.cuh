@@ -116,7 +116,7 @@ __device__ __forceinline__ F2 l1_chalf_x2(F2 c, F2 E, F2 W, F2 N, F2 S, F2 NE, F
 // as l1_energy_sums, with f from shared memory or (FG) global memory; each
 // thread adds its <= 7 pixels of a colour plane in fp32 (<= 6 ulp relative,
 // the size of the fp32 per-pixel terms) before the fp64 accumulators
-template <int TH, int TW, bool FG>
+template <int TH, int TW, bool FG, int NTH>
 __device__ __forceinline__ void x2_energy_sums(const float* su, const float* sf, const float* f, int R, int C,
                                                int m, int n, const float* up, const float* rf, double* partials,
                                                int b, int cta, int nbx) {
@@ -126,8 +126,13 @@ __device__ __forceinline__ void x2_energy_sums(const float* su, const float* sf,
     static_for<0, 4>([&](auto cp) {
         constexpr int P = decltype(cp)::value >> 1, Q = decltype(cp)::value & 1;
         float loc[NSUM] = {0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-        for (int t = threadIdx.x; t < CNT; t += blockDim.x) {
+        // unrolled: the global loads (u_prev, f) of all the thread's pixels of the
+        // plane are issued before their first use (a rolled loop pays one memory
+        // latency per pixel)
+#pragma unroll
+        for (int itr = 0; itr < (CNT + NTH - 1) / NTH; ++itr) {
+            const int t = threadIdx.x + itr * NTH;
+            if (t >= CNT) continue;
             const int ii = t / PW, kk = t % PW;
             const int gi = R + 2 * ii + P, gk = C + 2 * kk + Q;
             if (gi >= m || gk >= n) continue;
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     __syncthreads();
     if (border) l1_reflect_fix<float, TH, TW>(su, r0, c0, m, n);
     if (a.efuse)
-        x2_energy_sums<TH, TW, FG>(su, sf, f, R, C, m, n, a.uprev + (long long)b * a.istride,
+        x2_energy_sums<TH, TW, FG, NT>(su, sf, f, R, C, m, n, a.uprev + (long long)b * a.istride,
                                    a.ref ? a.ref + (long long)b * a.istride : nullptr, a.partials, b, cta, nbx);
     const F2 w2 = f2_splat((float)a.P->w[1][0]);
     const F2 inv2 = f2_splat((float)(1.0 / a.P->den[1][0]));
