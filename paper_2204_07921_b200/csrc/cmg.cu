@@ -700,7 +700,11 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     // packed k_l1_x2 kernel and the separate bulk energy pass) sums the energy of its
     // input; partials per level-1 CTA (tiles >= 32 x 32)
     {
-        P->efuse = P->fused && P->fused_finalize;
+        // packed fp32 level-1 kernel (k_l1_x2): only for latency-bound (small) jobs; on
+        // large ones the issue-heavy packed kernel pays more for the energy terms than the
+        // streamlined bulk energy pass costs (16384^2: 2.06 ms vs 0.90 + 0.56 ms)
+        const bool x2 = dtype == CMG_F32 && P->prec == CMG_PREC_FAST && mode == CMG_MODE_MEAN && P->l1x2;
+        P->efuse = P->fused && P->fused_finalize && (!x2 || small_job);
         if (const char* ef = getenv("CMG_EFUSE")) P->efuse = P->efuse && atoi(ef) != 0;
     }
     const long long l1tiles = (long long)((m + 31) / 32) * ((n + 31) / 32);
