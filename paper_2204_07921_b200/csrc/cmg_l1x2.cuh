@@ -161,7 +161,7 @@ __device__ __forceinline__ void x2_energy_sums(const float* su, const float* sf,
 
 // FG: f is not staged in shared memory but read from global memory (L2) by
 // the pixel's own phase: half the shared memory per CTA, more CTAs per SM
-template <int TH, int TW, int NR, bool FAST = true, int NT = 256, bool FG = false>
+template <int TH, int TW, int NR, bool FAST = true, int NT = 256, bool FG = false, bool EF = false>
 __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     pdl_sync();
     using G = L1Geom<float, TH, TW>;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     const int m = a.m, n = a.n;
     const int cta = blockIdx.y * gridDim.x + blockIdx.x, nbx = gridDim.x * gridDim.y;
     if (a.st[b].done) {  // stopped image (final u in ImgState::final_buf)
-        if (a.efuse) efused_ticket(a.fz, a.partials, nbx, b, reinterpret_cast<double*>(smem_raw));
+        if constexpr (EF) efused_ticket(a.fz, a.partials, nbx, b, reinterpret_cast<double*>(smem_raw));
         return;
     }
     const int r0 = R - G::HALO, c0 = C - G::HALO;
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     }
     __syncthreads();
     if (border) l1_reflect_fix<float, TH, TW>(su, r0, c0, m, n);
-    if (a.efuse)
+    if constexpr (EF)
         x2_energy_sums<TH, TW, FG, NT>(su, sf, f, R, C, m, n, a.uprev + (long long)b * a.istride,
                                    a.ref ? a.ref + (long long)b * a.istride : nullptr, a.partials, b, cta, nbx);
     const F2 w2 = f2_splat((float)a.P->w[1][0]);
@@ -444,12 +444,12 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     f2_unpack(finite_acc, fa0, fa1);
     const bool bad = !(isfinite(fa0) && isfinite(fa1));
     if (__syncthreads_or(bad) && threadIdx.x == 0) {
-        if (a.efuse)
+        if constexpr (EF)
             a.st[b].bad1 = 1;
         else
             a.st[b].bad = 1;
     }
-    if (a.efuse) {
+    if constexpr (EF) {
         __syncthreads();  // shared memory becomes the finalize scratch
         efused_ticket(a.fz, a.partials, nbx, b, reinterpret_cast<double*>(smem_raw));
     }

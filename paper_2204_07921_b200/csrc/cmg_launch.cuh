@@ -294,19 +294,27 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
             using I120 = std::integral_constant<int, 120>;
             using I88 = std::integral_constant<int, 88>;
             // 1: interior fast path (default), 2: Newton rsqrt on the diagonals, 3: generic loop only,
-            // 4: 56 x 120 tiles, 5: 88 x 88 tiles (192 threads)
-            switch (P->l1x2) {
-                case 2: go(k_l1_x2<56, 56, 1>, I56{}, I56{}, 256); break;
-                case 3: go(k_l1_x2<56, 56, 0, false>, I56{}, I56{}, 256); break;
-                case 4: go(k_l1_x2<56, 120, 0>, I56{}, I120{}, 256); break;
-                case 5: go(k_l1_x2<88, 88, 0, true, 192>, I88{}, I88{}, 192); break;
-                case 6: go(k_l1_x2<56, 120, 0, false>, I56{}, I120{}, 256); break;
-                case 7: go(k_l1_x2<56, 120, 0, true, 512>, I56{}, I120{}, 512); break;
-                case 8: go(k_l1_x2<120, 56, 0>, I120{}, I56{}, 256); break;
-                case 11: go(k_l1_x2<56, 120, 0, true, 256, true>, I56{}, I120{}, 256); break;
-                case 12: go(k_l1_x2<56, 56, 0, true, 256, true>, I56{}, I56{}, 256); break;
-                default: go(k_l1_x2<56, 56, 0>, I56{}, I56{}, 256); break;
-            }
+            // 4: 56 x 120 tiles, 5: 88 x 88 tiles (192 threads), 11 / 12: f read from global memory;
+            // EF: the energy-fused instantiation (its extra registers stay out of the plain one)
+            auto sel = [&](auto ef) {
+                constexpr bool EF = decltype(ef)::value;
+                switch (P->l1x2) {
+                    case 2: go(k_l1_x2<56, 56, 1, true, 256, false, EF>, I56{}, I56{}, 256); break;
+                    case 3: go(k_l1_x2<56, 56, 0, false, 256, false, EF>, I56{}, I56{}, 256); break;
+                    case 4: go(k_l1_x2<56, 120, 0, true, 256, false, EF>, I56{}, I120{}, 256); break;
+                    case 5: go(k_l1_x2<88, 88, 0, true, 192, false, EF>, I88{}, I88{}, 192); break;
+                    case 6: go(k_l1_x2<56, 120, 0, false, 256, false, EF>, I56{}, I120{}, 256); break;
+                    case 7: go(k_l1_x2<56, 120, 0, true, 512, false, EF>, I56{}, I120{}, 512); break;
+                    case 8: go(k_l1_x2<120, 56, 0, true, 256, false, EF>, I120{}, I56{}, 256); break;
+                    case 11: go(k_l1_x2<56, 120, 0, true, 256, true, EF>, I56{}, I120{}, 256); break;
+                    case 12: go(k_l1_x2<56, 56, 0, true, 256, true, EF>, I56{}, I56{}, 256); break;
+                    default: go(k_l1_x2<56, 56, 0, true, 256, false, EF>, I56{}, I56{}, 256); break;
+                }
+            };
+            if (a.efuse)
+                sel(std::true_type{});
+            else
+                sel(std::false_type{});
             return;
         }
     }
