@@ -427,6 +427,35 @@ void launch_rowpair(cmg_plan* P, const T* X, T* Y) {
     }
 }
 
+// the same launches with bulk-copy staging and bulk-store write-back
+// (k_rowpair_tma; n*sizeof(T) % 16 == 0)
+template <typename T, int LAYER, int MODE, int PREC, int TS, int NT = 256>
+void launch_rowpair_tma(cmg_plan* P, const T* X, T* Y) {
+    using G = RowPairGeom<LAYER, TS, NT, 16 / (int)sizeof(T)>;
+    const Level& L = P->lv[LAYER];
+    RowPairArgs<T> r;
+    r.X = X;
+    r.Y = Y;
+    r.nj = L.nj;
+    r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
+    const bool fs = P->fsum[LAYER] != nullptr && MODE == MODE_MEAN && PREC == PREC_FAST;
+    const size_t smem = sizeof(T) * (G::ROWS + (fs ? 0 : G::S)) * G::WIN;
+    auto kern = k_rowpair_tma<T, LAYER, MODE, PREC, TS, NT>;
+    smem_attr(kern, smem);
+    for (int p = 0; p < 2; ++p) {
+        const int rows = (L.mj - p + 1) / 2;
+        if (rows <= 0) continue;
+        r.c0 = make_sweep_args<T>(P, LAYER, 2 * p);
+        r.c1 = make_sweep_args<T>(P, LAYER, 2 * p + 1);
+        klaunch(P, kern, dim3(r.ntiles, rows, P->B), G::NT, smem, r);
+        if (p == 0) {
+            stamp(P, 10 * LAYER + 8);
+        } else {
+            P->enq += 1;  // the caller counts one launch per level
+        }
+    }
+}
+
 // persistent bulk-copy variant (one thread per patch, fast mean + f sums)
 template <typename T, int LAYER, int NT, int STAGES>
 void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y) {
@@ -500,6 +529,20 @@ void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
         }
     }
     // team sizes: level 2 {4, 8} lanes per patch (P->rp_ts2), level 3 {8, 16}
+    if (P->rp_tma && ((size_t)P->n * sizeof(T)) % 16 == 0) {
+        if (layer == 2) {
+            if (P->rp_ts2 >= 8)
+                launch_rowpair_tma<T, 2, MODE, PREC, 8>(P, a.uin, a.uout);
+            else
+                launch_rowpair_tma<T, 2, MODE, PREC, 4>(P, a.uin, a.uout);
+        } else {
+            if (P->ts3 >= 16)
+                launch_rowpair_tma<T, 3, MODE, PREC, 16>(P, a.uin, a.uout);
+            else
+                launch_rowpair_tma<T, 3, MODE, PREC, 8>(P, a.uin, a.uout);
+        }
+        return;
+    }
     if (layer == 2) {
         if (P->rp_ts2 >= 8)
             launch_rowpair<T, 2, MODE, PREC, 8>(P, a.uin, a.uout);

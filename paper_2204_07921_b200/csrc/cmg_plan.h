@@ -87,6 +87,7 @@ struct cmg_plan {
     bool l1_wide = false;   // k_l1_tile with 32 x 64 tiles (CMG_L1_WIDE)
     int rp_ts2 = 4;         // lanes per patch of the level-2 row-parity kernel (CMG_RP_TS2)
     int rp1 = 0;            // bit j-2: level j's row-parity kernel runs one thread per patch (CMG_RP1)
+    int rp_tma = 1;         // k_rowpair with bulk-copy staging / bulk-store write-back (CMG_RP_TMA)
     int rp_bulk = 1;        // ... as the persistent bulk-copy kernel (CMG_RP_BULK)
     int rp_stages = 1;      // shared-memory stages of that kernel (CMG_RP_STAGES: 1 or 2; 1 = more CTAs per SM, faster)
     int rp_nt = 64;         // threads per CTA of that kernel (CMG_RP_NT: 32, 64 or 128 [fp32])

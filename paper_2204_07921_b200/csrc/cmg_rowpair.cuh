@@ -231,6 +231,8 @@ __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem
                 }
             }
         }
+        // the caller's bulk stores (async proxy) read what these threads wrote
+        if constexpr (EDGES_ONLY && q == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (q == 0 && it.border) refill();
     });
@@ -271,6 +273,66 @@ __global__ void __launch_bounds__(NT) k_rowpair(RowPairArgs<T> a) {
     rp_stage<T, LAYER, TS, NT>(a, it, win);
     __syncthreads();
     rp_compute<T, LAYER, MODE, PREC, TS, NT>(a, it, win);
+}
+
+// ---------------------------------------------------------------------------
+// k_rowpair with bulk-copy staging (latency-bound jobs: config 3's levels 2-3).
+// One item per CTA as in k_rowpair, but the window rows (u rows R0-1 .. R0+S,
+// then the f rows R0 .. R0+S-1) arrive by one cp.async.bulk each, issued by
+// the lanes of warp 0 and completed on one mbarrier, and the A-aligned
+// interior of the owned rows leaves by bulk stores: the per-column staging and
+// write-back loops (40 % of k_rowpair's instructions at level 3) disappear.
+// The window origin is floored to A = 16/sizeof(T) columns so shared-memory
+// and global columns share their 16-byte phase.  Requires n*sizeof(T) % 16 == 0.
+// ---------------------------------------------------------------------------
+template <typename T, int LAYER, int MODE, int PREC, int TS, int NT = 256>
+__global__ void __launch_bounds__(NT) k_rowpair_tma(RowPairArgs<T> a) {
+    pdl_sync();
+    constexpr int A = 16 / (int)sizeof(T);
+    using G = RowPairGeom<LAYER, TS, NT, A>;
+    constexpr int S = G::S;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* win = reinterpret_cast<T*>(smem_raw);
+    __shared__ __align__(8) unsigned long long full;
+    const int m = a.c0.m, n = a.c0.n, p = a.c0.p;
+    RPItem<T> it = rp_item<T, LAYER, TS, NT>(a, blockIdx.z, blockIdx.y, blockIdx.x);
+    it.wk0 = (it.wk0 >= 0) ? (it.wk0 / A) * A : -(((-it.wk0) + A - 1) / A) * A;
+    it.border = (it.wr0 < 0) || (it.wr0 + G::ROWS > m) || (it.wk0 < 0) || (it.wk0 + G::WIN > n);
+    const bool fs = a.c0.fsum != nullptr;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int wlo = max(it.wk0, 0), whi = min(it.wk0 + G::WIN, n);
+        const unsigned bytes = (unsigned)(whi - wlo) * (unsigned)sizeof(T);
+        // lane r < ROWS: u row wr0 + r; ROWS <= r < ROWS + S: f row R0 + r - ROWS
+        const int nr = G::ROWS + (fs ? 0 : S);
+        const int i = lane < G::ROWS ? it.wr0 + lane : it.R0 + (lane - G::ROWS);
+        const bool valid = lane < nr && i >= 0 && i < m;
+        const unsigned cnt = __popc(__ballot_sync(0xffffffffu, valid));
+        if (lane == 0) {
+            mbar_init(&full, 1);
+            mbar_expect_tx(&full, bytes * cnt);
+        }
+        __syncwarp();
+        if (valid) {
+            const T* src = lane < G::ROWS ? rp_src_row<T, S>(it, p, i) : it.f;
+            bulk_g2s(win + lane * G::WIN + (wlo - it.wk0), src + (long long)i * n + wlo, bytes, &full);
+        }
+    }
+    const bool done = a.c0.st[it.b].done != 0;
+    __syncthreads();  // barrier initialised
+    mbar_wait(&full, 0u);
+    if (done) return;  // stopped image (final u in ImgState::final_buf); the copies have landed
+    rp_compute<T, LAYER, MODE, PREC, TS, NT, A, true>(a, it, win);
+    if (threadIdx.x == 0) {
+        const int a0 = min(((it.ok0 + A - 1) / A) * A, it.ok1), a1 = max((it.ok1 / A) * A, a0);
+        if (a1 > a0) {
+            for (int i = it.R0; i < it.orow1; ++i)
+                bulk_s2g(it.Yb + (long long)i * n + a0, win + (i - it.wr0) * G::WIN + (a0 - it.wk0),
+                         (unsigned)(a1 - a0) * (unsigned)sizeof(T));
+            bulk_commit();
+            bulk_wait_read0();  // shared memory stays valid until the stores have read it
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
