@@ -206,6 +206,17 @@ int cmg_host_free(void* p);
 int cmg_l2_read_bandwidth(int device, long long bytes, int reps, double* gbs);
 
 /*
+ * Self test (no reference counterpart) of the branch-free correctly rounded
+ * fp64 sqrt / div that the level-1 exact kernel uses (csrc/cmg_l1loop.cuh)
+ * against the device library's sqrt.rn / div.rn on n host operand pairs:
+ * out[0] / out[1] = in-range sqrt(a[i]) / (a[i] / b[i]) results that differ
+ * from the library (must be 0), out[2] / out[3] = operands whose range test
+ * selects the library path.
+ */
+int cmg_selftest_exact(int device, const double* a_host, const double* b_host, long long n,
+                       unsigned long long* out);
+
+/*
  * Curvature-regularised reconstruction (curvemg.reconstruction, fp64, device
  * pointers, work enqueued on `stream`; paper_2204_07921_b200.recon drives
  * them).  Parallel-beam Radon operator (reconstruction.py:123-183): the

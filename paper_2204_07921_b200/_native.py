@@ -25,6 +25,7 @@ SYMBOLS = (
     "cmg_solve_device", "cmg_sweep_layer", "cmg_energy", "cmg_plane_table", "cmg_plan_stats", "cmg_time_sweep",
     "cmg_host_alloc", "cmg_host_free", "cmg_plan_buffer", "cmg_buffer_upload", "cmg_buffer_download",
     "cmg_level_step", "cmg_energy_partials", "cmg_ssim_batch", "cmg_plan_ssim", "cmg_l2_read_bandwidth",
+    "cmg_selftest_exact",
     "cmg_plan_stream", "cmg_strip_begin", "cmg_level_step_async", "cmg_strip_partials_async", "cmg_strip_read",
     "cmg_mplan_create", "cmg_mplan_destroy", "cmg_mplan_solve",
     "cmg_radon_create", "cmg_radon_destroy", "cmg_radon_forward", "cmg_radon_adjoint", "cmg_recon_chalf",
@@ -106,6 +107,8 @@ def _declare(L):
     L.cmg_strip_read.argtypes = [_vp, _dp]
     L.cmg_l2_read_bandwidth.restype = _i
     L.cmg_l2_read_bandwidth.argtypes = [_i, ctypes.c_longlong, _i, _dp]
+    L.cmg_selftest_exact.restype = _i
+    L.cmg_selftest_exact.argtypes = [_i, _dp, _dp, ctypes.c_longlong, ctypes.POINTER(ctypes.c_ulonglong)]
     L.cmg_host_free.restype = _i
     L.cmg_host_free.argtypes = [_vp]
     L.cmg_plan_buffer.restype = _i
@@ -217,6 +220,21 @@ def l2_read_bandwidth(device: int = 0, nbytes: int = 32 << 20, reps: int = 50) -
     if rc != CMG_OK:
         raise RuntimeError(last_error())
     return out.value
+
+
+def selftest_exact(a, b, device: int = 0):
+    """cmg_selftest_exact: (sqrt mismatches, div mismatches, sqrt out-of-range, div out-of-range) of the
+    branch-free correctly rounded sqrt(a) and a / b against the device library."""
+    import numpy as np
+
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    assert a.shape == b.shape and a.ndim == 1
+    out = (ctypes.c_ulonglong * 4)()
+    rc = lib().cmg_selftest_exact(device, a.ctypes.data_as(_dp), b.ctypes.data_as(_dp), a.size, out)
+    if rc != CMG_OK:
+        raise RuntimeError(f"cmg_selftest_exact failed ({rc})")
+    return tuple(int(x) for x in out)
 
 
 class MPlan:

@@ -708,7 +708,7 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
         P->efuse = P->fused && P->fused_finalize && (!x2 || small_job);
         if (const char* ef = getenv("CMG_EFUSE")) P->efuse = P->efuse && atoi(ef) != 0;
     }
-    const long long l1tiles = (long long)((m + 31) / 32) * ((n + 31) / 32);
+    const long long l1tiles = (long long)((m + 27) / 28) * ((n + 31) / 32);  // covers 28-row tiles too
     const long long nparts = std::max<long long>(P->nbx, P->efuse ? l1tiles : 0);
     CKP(cudaMalloc(&P->partials, sizeof(double) * NSUM * (size_t)nparts * batch));
     P->pcap = (int)(nparts * batch);
@@ -724,6 +724,25 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
     // 4096^2: 643 -> 579 us; 512^2 has too few: 20.3 -> 27.2 us)
     P->l1_wide = (long long)batch * m * n >= (1LL << 20);
     if (const char* lw = getenv("CMG_L1_WIDE")) P->l1_wide = atoi(lw) != 0;
+    if (dtype == CMG_F64) {
+        // fp64 level-1 tile shape: the kernel runs 4 CTAs of 256 threads per SM and its
+        // duration is that of the fullest SM, so pick the shape with the least
+        // (CTA waves) x (pixels a CTA relaxes, halo included).  1024^2: 28 x 64 tiles
+        // = 37 x 16 = 592 CTAs = exactly 4 per SM (level-1 sweep 45.6 -> 40.8 us).
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+        const long long slots = 4LL * nsm;
+        auto cost = [&](int th, int tw) {
+            const long long g = (long long)((m + th - 1) / th) * ((n + tw - 1) / tw) * batch;
+            return ((g + slots - 1) / slots) * (long long)(th + 6) * (tw + 6);
+        };
+        const long long c32 = cost(32, 32), c64 = cost(32, 64), c28 = cost(28, 64);
+        P->l1_wide = c64 < c32;
+        P->l1_th = (c28 < c64 && c28 < c32) ? 28 : 0;
+        if (const char* lw = getenv("CMG_L1_WIDE")) P->l1_wide = atoi(lw) != 0;
+    }
+    if (const char* lt = getenv("CMG_L1_TH")) P->l1_th = atoi(lt);
+    if (const char* ll = getenv("CMG_L1_LOOP")) P->l1_loop = atoi(ll);
     if (const char* en = getenv("CMG_ENERGY_NT")) P->energy_nt = atoi(en) == 512 ? 512 : 256;
     CKP(cudaMalloc(&P->P, sizeof(SolveParams)));
 #undef CKP

@@ -245,8 +245,17 @@ __device__ __forceinline__ void l1_energy_sums(const T* su, const T* sf, int R, 
     cta_sums_store(acc, partials, nbx, cta, b);
 }
 
+// plane-loop exact correction (cmg_l1loop.cuh)
+template <int TH, int TW, int C>
+__device__ __forceinline__ double l1_correction_loop(const double* sp, double fval, double w, double den);
+template <int TH, int TW, int C>
+__device__ __forceinline__ double l1_correction_unrolled(const double* sp, double fval, double w, double den,
+                                                         unsigned guard);
+
 // (mean mode: 4 CTAs of 256 threads per SM, <= 64 registers)
-template <typename T, int MODE, int PREC, int TH, int TW>
+// LOOP: fp64 exact mean mode with one inner iteration and no single-patch colour
+// class -- the plane-loop pixel code of cmg_l1loop.cuh
+template <typename T, int MODE, int PREC, int TH, int TW, int LOOP = 0>
 __global__ void __launch_bounds__(256, MODE == MODE_MEAN ? 4 : 1) k_l1_tile(FusedArgs<T> a) {
     pdl_sync();
     using G = L1Geom<T, TH, TW>;
@@ -284,6 +293,8 @@ __global__ void __launch_bounds__(256, MODE == MODE_MEAN ? 4 : 1) k_l1_tile(Fuse
                                   a.ref ? a.ref + (long long)b * a.istride : nullptr, a.mode, a.partials, b, cta,
                                   nbx);
     bool bad = false;
+    // four always-set bits from unrelated runtime values (cmg_l1loop.cuh: plane-pair guards)
+    const unsigned guard = (m > 0 ? 1u : 0u) | (n > 0 ? 2u : 0u) | (a.istride >= 0 ? 4u : 0u) | (nbx > 0 ? 8u : 0u);
     L1Back<T> bk;
     bk.P = a.P;
     bk.inner = a.P->inner;
@@ -319,7 +330,13 @@ __global__ void __launch_bounds__(256, MODE == MODE_MEAN ? 4 : 1) k_l1_tile(Fuse
                 if (ok) {
                     QuadAcc<T, TH, TW, P, Q> A{su, qi, qk};
                     const int sidx = (P * 2 + Q) * G::PLANE + qi * G::QW + qk;
-                    const T corr = l1_correction<T, TH, TW, P, Q, MODE, PREC>(A, sf[sidx], bk, single);
+                    T corr;
+                    if constexpr (LOOP == 1)
+                        corr = l1_correction_loop<TH, TW, c>(su + qi * G::QW + qk, sf[sidx], bk.w, bk.den);
+                    else if constexpr (LOOP == 2)
+                        corr = l1_correction_unrolled<TH, TW, c>(su + qi * G::QW + qk, sf[sidx], bk.w, bk.den, guard);
+                    else
+                        corr = l1_correction<T, TH, TW, P, Q, MODE, PREC>(A, sf[sidx], bk, single);
                     bad |= !isfinite(corr);
                     su[sidx] = X<T>::add(su[sidx], corr);
                 }

@@ -10,6 +10,7 @@
 #include "cmg_fused.cuh"
 #include "cmg_l1.cuh"
 #include "cmg_l1x2.cuh"
+#include "cmg_l1loop.cuh"
 #include "cmg_coarse.cuh"
 #include "cmg_energy_bulk.cuh"
 #include "cmg_rowpair.cuh"
@@ -322,13 +323,35 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
         constexpr int TH = decltype(th)::value, TW = decltype(tw)::value;
         using G = L1Geom<T, TH, TW>;
         const size_t smem = 2 * sizeof(T) * 4 * G::PLANE;
+        const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
+        if constexpr (std::is_same<T, double>::value && MODE == MODE_MEAN && PREC == PREC_EXACT) {
+            // plane-loop pixel code: one inner iteration, sequential plane mean (no
+            // single-patch colour class: images of 4+ pixels per side)
+            if (P->l1_loop && P->hostP.inner == 1 && P->m >= 4 && P->n >= 4) {
+                if (P->l1_loop == 1) {
+                    auto kern = k_l1_tile<T, MODE, PREC, TH, TW, 1>;
+                    smem_attr(kern, smem);
+                    klaunch(P, kern, grd, 256, smem, a);
+                } else {
+                    auto kern = k_l1_tile<T, MODE, PREC, TH, TW, 2>;
+                    smem_attr(kern, smem);
+                    klaunch(P, kern, grd, 256, smem, a);
+                }
+                return;
+            }
+        }
         auto kern = k_l1_tile<T, MODE, PREC, TH, TW>;
         smem_attr(kern, smem);
-        const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
         klaunch(P, kern, grd, 256, smem, a);
     };
     using IH = std::integral_constant<int, L1Tile<T>::TH>;
     using IW = std::integral_constant<int, L1Tile<T>::TW>;
+    if constexpr (std::is_same<T, double>::value) {
+        if (P->l1_th == 28) {  // 28 x 64 tiles: 37 x 16 = 592 CTAs = 4 per SM at 1024^2
+            go(std::integral_constant<int, 28>{}, std::integral_constant<int, 64>{});
+            return;
+        }
+    }
     if (P->l1_wide)  // 32 x 64 tiles: fewer CTAs (one wave at 1024^2 fp64), less halo per pixel
         go(std::integral_constant<int, 32>{}, std::integral_constant<int, 64>{});
     else

@@ -37,6 +37,10 @@ VARIANTS = {
     "row_parity_ldg_staging_8_8": {"CMG_ROWPAIR": "3", "CMG_RP_TMA": "0", "CMG_RP_TS2": "8", "CMG_TS3": "8"},
     "no_programmatic_launch": {"CMG_PDL": "0"},
     "level1_wide_tiles": {"CMG_L1_WIDE": "1"},
+    "level1_library_sqrt_div": {"CMG_L1_LOOP": "0"},
+    "level1_plane_loop": {"CMG_L1_LOOP": "1"},
+    "level1_plane_loop_wide_tiles": {"CMG_L1_LOOP": "1", "CMG_L1_WIDE": "1"},
+    "level1_unrolled_wide_tiles": {"CMG_L1_LOOP": "2", "CMG_L1_WIDE": "1"},
     "energy_256_threads": {"CMG_ENERGY_NT": "256"},
     "energy_separate_pass": {"CMG_EFUSE": "0"},
     "energy_separate_pass_per_colour": {"CMG_EFUSE": "0", "CMG_ROWPAIR": "0"},

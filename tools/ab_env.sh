@@ -7,5 +7,5 @@ for e in "$@"; do
   i=$((i+1))
   env $e timeout 300 python bench.py --no-cpu --no-fine > $O/b_$i.json 2>$O/b_$i.err
   python -c "
-import json;d=json.load(open('$O/b_$i.json'));print('$e', round(d['ms_per_step'],3), {k:round(v*1000,1) for k,v in d['detail']['level_sweep_ms'].items()}, {k:round(v['time_to_tolerance_ms'],3) for k,v in d['detail']['other_precisions'].items()})" || tail -3 $O/b_$i.err
+import json;d=json.load(open('$O/b_$i.json'));print('$e', round(d['ms_per_step'],3), {k:round(v*1000,1) for k,v in d['detail']['level_sweep_ms'].items()})" || tail -3 $O/b_$i.err
 done
