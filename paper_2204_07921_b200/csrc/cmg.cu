@@ -742,7 +742,7 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
         if (const char* lw = getenv("CMG_L1_WIDE")) P->l1_wide = atoi(lw) != 0;
     }
     if (const char* lt = getenv("CMG_L1_TH")) P->l1_th = atoi(lt);
-    if (const char* ll = getenv("CMG_L1_LOOP")) P->l1_loop = atoi(ll);
+    if (const char* ll = getenv("CMG_L1_LOOP")) P->l1_loop = atoi(ll) != 0;
     if (const char* en = getenv("CMG_ENERGY_NT")) P->energy_nt = atoi(en) == 512 ? 512 : 256;
     CKP(cudaMalloc(&P->P, sizeof(SolveParams)));
 #undef CKP

@@ -245,17 +245,15 @@ __device__ __forceinline__ void l1_energy_sums(const T* su, const T* sf, int R, 
     cta_sums_store(acc, partials, nbx, cta, b);
 }
 
-// plane-loop exact correction (cmg_l1loop.cuh)
-template <int TH, int TW, int C>
-__device__ __forceinline__ double l1_correction_loop(const double* sp, double fval, double w, double den);
+// branch-free exact correction (cmg_l1loop.cuh)
 template <int TH, int TW, int C>
 __device__ __forceinline__ double l1_correction_unrolled(const double* sp, double fval, double w, double den,
                                                          unsigned guard);
 
 // (mean mode: 4 CTAs of 256 threads per SM, <= 64 registers)
 // LOOP: fp64 exact mean mode with one inner iteration and no single-patch colour
-// class -- the plane-loop pixel code of cmg_l1loop.cuh
-template <typename T, int MODE, int PREC, int TH, int TW, int LOOP = 0>
+// class -- the branch-free pixel code of cmg_l1loop.cuh
+template <typename T, int MODE, int PREC, int TH, int TW, bool LOOP = false>
 __global__ void __launch_bounds__(256, MODE == MODE_MEAN ? 4 : 1) k_l1_tile(FusedArgs<T> a) {
     pdl_sync();
     using G = L1Geom<T, TH, TW>;
@@ -275,18 +273,52 @@ __global__ void __launch_bounds__(256, MODE == MODE_MEAN ? 4 : 1) k_l1_tile(Fuse
         return;
     }
     const int r0 = R - G::HALO, c0 = C - G::HALO;
-    // stage u and f (in-image cells of the region)
-    for (int e = threadIdx.x; e < G::RH * G::RW; e += blockDim.x) {
-        const int i = e / G::RW, k = e % G::RW;
-        const int gi = r0 + i, gk = c0 + k;
-        if (gi >= 0 && gi < m && gk >= 0 && gk < n) {
-            const long long g = (long long)gi * n + gk;
-            su[G::idx(i, k)] = uin[g];
-            sf[G::idx(i, k)] = f[g];
+    const bool border = (r0 < 1) || (c0 < 1) || (r0 + G::RH >= m) || (c0 + G::RW >= n);
+    // stage u and f
+    if (!border && (n & 1) == 0) {
+        // interior tile: every load of the thread (column pairs, 2 x sizeof(T) bytes) is
+        // issued before the first shared-memory store -- one memory round trip instead
+        // of one per element (the bounds-checked loop below serialises them)
+        struct alignas(2 * sizeof(T)) Pair {
+            T a, b;
+        };
+        constexpr int PW = G::RW / 2, PAIRS = G::RH * PW, IT = (PAIRS + 255) / 256;
+        Pair vu[IT], vf[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int e = threadIdx.x + it * 256;
+            if (PAIRS % 256 == 0 || it + 1 < IT || e < PAIRS) {
+                const int i = e / PW, kp = e % PW;
+                const long long g = (long long)(r0 + i) * n + c0 + 2 * kp;
+                vu[it] = *reinterpret_cast<const Pair*>(uin + g);
+                vf[it] = *reinterpret_cast<const Pair*>(f + g);
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int e = threadIdx.x + it * 256;
+            if (PAIRS % 256 == 0 || it + 1 < IT || e < PAIRS) {
+                const int i = e / PW, kp = e % PW;
+                const int base = ((i & 1) * 2) * G::PLANE + (i >> 1) * G::QW + kp;  // idx(i, 2 kp)
+                su[base] = vu[it].a;
+                su[base + G::PLANE] = vu[it].b;
+                sf[base] = vf[it].a;
+                sf[base + G::PLANE] = vf[it].b;
+            }
+        }
+    } else {
+        // border tile: in-image cells of the region
+        for (int e = threadIdx.x; e < G::RH * G::RW; e += blockDim.x) {
+            const int i = e / G::RW, k = e % G::RW;
+            const int gi = r0 + i, gk = c0 + k;
+            if (gi >= 0 && gi < m && gk >= 0 && gk < n) {
+                const long long g = (long long)gi * n + gk;
+                su[G::idx(i, k)] = uin[g];
+                sf[G::idx(i, k)] = f[g];
+            }
         }
     }
     __syncthreads();
-    const bool border = (r0 < 1) || (c0 < 1) || (r0 + G::RH >= m) || (c0 + G::RW >= n);
     if (border) l1_reflect_fix<T, TH, TW>(su, r0, c0, m, n);
     if (a.efuse)
         l1_energy_sums<T, TH, TW>(su, sf, R, C, m, n, a.uprev + (long long)b * a.istride,
@@ -331,9 +363,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_MEAN ? 4 : 1) k_l1_tile(Fuse
                     QuadAcc<T, TH, TW, P, Q> A{su, qi, qk};
                     const int sidx = (P * 2 + Q) * G::PLANE + qi * G::QW + qk;
                     T corr;
-                    if constexpr (LOOP == 1)
-                        corr = l1_correction_loop<TH, TW, c>(su + qi * G::QW + qk, sf[sidx], bk.w, bk.den);
-                    else if constexpr (LOOP == 2)
+                    if constexpr (LOOP)
                         corr = l1_correction_unrolled<TH, TW, c>(su + qi * G::QW + qk, sf[sidx], bk.w, bk.den, guard);
                     else
                         corr = l1_correction<T, TH, TW, P, Q, MODE, PREC>(A, sf[sidx], bk, single);

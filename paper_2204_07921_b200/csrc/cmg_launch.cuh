@@ -325,18 +325,12 @@ void launch_l1_tile(cmg_plan* P, const FusedArgs<T>& a) {
         const size_t smem = 2 * sizeof(T) * 4 * G::PLANE;
         const dim3 grd((P->n + TW - 1) / TW, (P->m + TH - 1) / TH, P->B);
         if constexpr (std::is_same<T, double>::value && MODE == MODE_MEAN && PREC == PREC_EXACT) {
-            // plane-loop pixel code: one inner iteration, sequential plane mean (no
+            // branch-free pixel code (cmg_l1loop.cuh): one inner iteration, sequential plane mean (no
             // single-patch colour class: images of 4+ pixels per side)
             if (P->l1_loop && P->hostP.inner == 1 && P->m >= 4 && P->n >= 4) {
-                if (P->l1_loop == 1) {
-                    auto kern = k_l1_tile<T, MODE, PREC, TH, TW, 1>;
-                    smem_attr(kern, smem);
-                    klaunch(P, kern, grd, 256, smem, a);
-                } else {
-                    auto kern = k_l1_tile<T, MODE, PREC, TH, TW, 2>;
-                    smem_attr(kern, smem);
-                    klaunch(P, kern, grd, 256, smem, a);
-                }
+                auto kern = k_l1_tile<T, MODE, PREC, TH, TW, true>;
+                smem_attr(kern, smem);
+                klaunch(P, kern, grd, 256, smem, a);
                 return;
             }
         }

@@ -86,8 +86,8 @@ struct cmg_plan {
     int rowpair = 3;        // bit j-2: level j (2, 3) runs as two row-parity launches (k_rowpair)
     bool l1_wide = false;   // k_l1_tile with 32 x 64 tiles (CMG_L1_WIDE)
     int l1_th = 0;          // fp64 level-1 tile height override (CMG_L1_TH=28: 28 x 64 tiles)
-    int l1_loop = 2;        // fp64 exact mean level 1 with branch-free sqrt/div (CMG_L1_LOOP): 0 library
-                            // pixel code, 1 table-driven plane loop, 2 compile-time planes
+    bool l1_loop = true;    // fp64 exact mean level 1: branch-free sqrt/div pixel code of cmg_l1loop.cuh
+                            // (CMG_L1_LOOP=0: library sqrt/div)
     int rp_ts2 = 4;         // lanes per patch of the level-2 row-parity kernel (CMG_RP_TS2)
     int rp1 = 0;            // bit j-2: level j's row-parity kernel runs one thread per patch (CMG_RP1)
     int rp_tma = 1;         // k_rowpair with bulk-copy staging / bulk-store write-back (CMG_RP_TMA)

@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(NT) k_rowpair(RowPairArgs<T> a) {
 template <typename T, int LAYER, int MODE, int PREC, int TS, int NT = 256>
 __global__ void __launch_bounds__(NT) k_rowpair_tma(RowPairArgs<T> a) {
     pdl_sync();
+    if (a.c0.dbg & 8) return;  // diagnostics: launch cost only
     constexpr int A = 16 / (int)sizeof(T);
     using G = RowPairGeom<LAYER, TS, NT, A>;
     constexpr int S = G::S;
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(NT) k_rowpair_tma(RowPairArgs<T> a) {
     __syncthreads();  // barrier initialised
     mbar_wait(&full, 0u);
     if (done) return;  // stopped image (final u in ImgState::final_buf); the copies have landed
+    if (a.c0.dbg & 16) return;  // diagnostics: launch + staging
     rp_compute<T, LAYER, MODE, PREC, TS, NT, A, true>(a, it, win);
     if (threadIdx.x == 0) {
         const int a0 = min(((it.ok0 + A - 1) / A) * A, it.ok1), a1 = max((it.ok1 / A) * A, a0);

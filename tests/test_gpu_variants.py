@@ -38,9 +38,9 @@ VARIANTS = {
     "no_programmatic_launch": {"CMG_PDL": "0"},
     "level1_wide_tiles": {"CMG_L1_WIDE": "1"},
     "level1_library_sqrt_div": {"CMG_L1_LOOP": "0"},
-    "level1_plane_loop": {"CMG_L1_LOOP": "1"},
-    "level1_plane_loop_wide_tiles": {"CMG_L1_LOOP": "1", "CMG_L1_WIDE": "1"},
-    "level1_unrolled_wide_tiles": {"CMG_L1_LOOP": "2", "CMG_L1_WIDE": "1"},
+    "level1_branch_free_wide_tiles": {"CMG_L1_WIDE": "1", "CMG_L1_TH": "0"},
+    "level1_branch_free_28_row_tiles": {"CMG_L1_TH": "28"},
+    "level1_library_sqrt_div_28_row_tiles": {"CMG_L1_LOOP": "0", "CMG_L1_TH": "28"},
     "energy_256_threads": {"CMG_ENERGY_NT": "256"},
     "energy_separate_pass": {"CMG_EFUSE": "0"},
     "energy_separate_pass_per_colour": {"CMG_EFUSE": "0", "CMG_ROWPAIR": "0"},
