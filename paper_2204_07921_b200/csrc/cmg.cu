@@ -741,6 +741,7 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
         P->l1_th = (c28 < c64 && c28 < c32) ? 28 : 0;
         if (const char* lw = getenv("CMG_L1_WIDE")) P->l1_wide = atoi(lw) != 0;
     }
+    if (const char* rt = getenv("CMG_RP_TNT")) P->rp_tnt = atoi(rt);
     if (const char* lt = getenv("CMG_L1_TH")) P->l1_th = atoi(lt);
     if (const char* ll = getenv("CMG_L1_LOOP")) P->l1_loop = atoi(ll) != 0;
     if (const char* en = getenv("CMG_ENERGY_NT")) P->energy_nt = atoi(en) == 512 ? 512 : 256;

@@ -33,6 +33,7 @@ VARIANTS = {
     "row_parity_levels_2_3": {"CMG_ROWPAIR": "3"},
     "row_parity_team_sizes_8_8": {"CMG_ROWPAIR": "3", "CMG_RP_TS2": "8", "CMG_TS3": "8"},
     "row_parity_off": {"CMG_ROWPAIR": "0"},
+    "row_parity_level2_256_threads": {"CMG_RP_TNT": "256"},
     "row_parity_ldg_staging": {"CMG_ROWPAIR": "3", "CMG_RP_TMA": "0"},
     "row_parity_ldg_staging_8_8": {"CMG_ROWPAIR": "3", "CMG_RP_TMA": "0", "CMG_RP_TS2": "8", "CMG_TS3": "8"},
     "no_programmatic_launch": {"CMG_PDL": "0"},
