@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(256) k_sweep_team(SweepArgs<T> a) {
 // ---------------------------------------------------------------------------
 template <typename T, int MODE, class Acc>
 __device__ __forceinline__ void bpp_body(const Acc& U, const Acc& F, int R0, int C0, const SweepArgs<T>& a,
-                                         T* sh_rows, T* sh_vals, T* sh_c) {
+                                         T* sh_rows, T* sh_vals, T* sh_c, ArgBest<T>* sh_best) {
     using O = X<T>;
     const int S = a.s, NPL = 1 << (a.layer + 2);
     const int ci = R0 + a.r - 1, cc = C0 + a.r - 1;
@@ -521,17 +521,53 @@ __device__ __forceinline__ void bpp_body(const Acc& U, const Acc& F, int R0, int
     if (a.flat) {
         if (tid == 0) sh_rows[0] = pairwise_any<T>(S * S, [&](int e) { return D(e / S, e % S); });
     } else {
-        for (int aa = tid; aa < S; aa += blockDim.x)
-            sh_rows[aa] = pairwise_small<T>(S, [&](int bb) { return D(aa, bb); });
+        // row sums in numpy's pairwise order (8 <= S < 128: eight strided accumulators,
+        // a fixed combination tree, then the remainder): eight lanes per row, lane t
+        // owns accumulator t, so a row's loads are coalesced and short
+        const int t = tid & 7, rg = tid >> 3, nrg = blockDim.x >> 3;
+        const int n8 = S - (S % 8);
+        for (int base = 0; base < S; base += nrg) {
+            const bool act = base + rg < S;
+            const int aa = act ? base + rg : S - 1;
+            T r = D(aa, t);
+            for (int i = 8; i < n8; i += 8) r = O::add(r, D(aa, i + t));
+            r = O::add(r, __shfl_down_sync(0xffffffffu, r, 1, 8));  // t even: r_t + r_{t+1}
+            r = O::add(r, __shfl_down_sync(0xffffffffu, r, 2, 8));  // t = 0, 4: pairs of pairs
+            r = O::add(r, __shfl_down_sync(0xffffffffu, r, 4, 8));  // t = 0: the tree's root
+            if (t == 0 && act) {
+                for (int i = n8; i < S; ++i) r = O::add(r, D(aa, i));
+                sh_rows[aa] = r;
+            }
+        }
     }
     const T uo = U(ci, cc);
     for (int l = tid; l < NPL; l += blockDim.x) {
         T v;
+        // lane-divergent plane index: the packed global table (constant memory would serialise)
         if (MODE == MODE_MEAN)
-            plane_exact_rt<T>(U, ci, cc, uo, PlaneRT::get(l), &v, nullptr);
+            plane_exact_rt<T>(U, ci, cc, uo, PlaneRT::getg(l), &v, nullptr);
         else
-            plane_exact_rt<T>(U, ci, cc, uo, PlaneRT::get(l), nullptr, &v);
+            plane_exact_rt<T>(U, ci, cc, uo, PlaneRT::getg(l), nullptr, &v);
         sh_vals[l] = v;
+    }
+    if (MODE != MODE_MEAN) {
+        // Gaussian mode: lexicographic (value, index, NaN) reductions of the thread's
+        // planes, then of the warp; thread 0 combines the warps
+        // (a thread or warp without a plane holds +-inf with the largest index, which loses
+        // against every plane: NaN beats it, any number is at least as good with a lower index)
+        ArgBest<T> bmin{T(INFINITY), 0x7fffffff, false}, bmax{T(-INFINITY), 0x7fffffff, false};
+        for (int l = tid; l < NPL; l += blockDim.x) {
+            const T v = sh_vals[l];  // this thread's own value
+            const ArgBest<T> c{v, l, (bool)isnan(v)};
+            bmin = arg_better<true>(bmin, c);
+            bmax = arg_better<false>(bmax, c);
+        }
+        bmin = arg_reduce<true, 32>(bmin);
+        bmax = arg_reduce<false, 32>(bmax);
+        if ((tid & 31) == 0) {
+            sh_best[2 * (tid >> 5)] = bmin;
+            sh_best[2 * (tid >> 5) + 1] = bmax;
+        }
     }
     __syncthreads();
     if (tid == 0) {
@@ -540,6 +576,7 @@ __device__ __forceinline__ void bpp_body(const Acc& U, const Acc& F, int R0, int
             acc = O::add(T(0), sh_rows[0]);
         } else {
             acc = T(0);
+#pragma unroll 8
             for (int aa = 0; aa < S; ++aa) acc = O::add(acc, sh_rows[aa]);
         }
         const T fstar = O::div(acc, T(S * S));
@@ -550,24 +587,18 @@ __device__ __forceinline__ void bpp_body(const Acc& U, const Acc& F, int R0, int
                 sum = pairwise_any<T>(NPL, [&](int i) { return sh_vals[i]; });
             } else {
                 sum = sh_vals[0];
+#pragma unroll 8
                 for (int l = 1; l < NPL; ++l) sum = O::add(sum, sh_vals[l]);
             }
             chalf = O::mul(sum, T(1.0 / NPL));  // NPL = 2^(J+2): exact reciprocal, same as the division
         } else {
-            int imin = 0, imax = 0;
-            if (!isnan(sh_vals[0])) {
-                for (int l = 1; l < NPL; ++l) {
-                    const T x = sh_vals[l];
-                    if (isnan(x)) {
-                        imin = l;
-                        imax = l;
-                        break;
-                    }
-                    if (x < sh_vals[imin]) imin = l;
-                    if (x > sh_vals[imax]) imax = l;
-                }
+            // np.argmin / np.argmax from the per-warp results (first NaN wins, ties -> lower index)
+            ArgBest<T> bmin = sh_best[0], bmax = sh_best[1];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+                bmin = arg_better<true>(bmin, sh_best[2 * w]);
+                bmax = arg_better<false>(bmax, sh_best[2 * w + 1]);
             }
-            const int star = (fabs(sh_vals[imin]) <= fabs(sh_vals[imax])) ? imin : imax;
+            const int star = (fabs(bmin.v) <= fabs(bmax.v)) ? bmin.i : bmax.i;
             plane_exact_rt<T>(U, ci, cc, uo, PlaneRT::get(star), &chalf, nullptr);
         }
         T c = T(0);
@@ -578,11 +609,12 @@ __device__ __forceinline__ void bpp_body(const Acc& U, const Acc& F, int R0, int
 }
 
 template <typename T, int MODE, int SRC>
-__global__ void __launch_bounds__(128) k_sweep_bpp(SweepArgs<T> a) {
+__global__ void __launch_bounds__(256) k_sweep_bpp(SweepArgs<T> a) {
     pdl_sync();
     __shared__ T sh_rows[64];
     __shared__ T sh_vals[256];
     __shared__ T sh_c;
+    __shared__ ArgBest<T> sh_best[16];  // per-warp argmin / argmax (Gaussian mode, <= 8 warps)
     const int b = blockIdx.z;
     if (a.st[b].done) return;
     const int pc = blockIdx.x, pr = blockIdx.y;
@@ -592,15 +624,15 @@ __global__ void __launch_bounds__(128) k_sweep_bpp(SweepArgs<T> a) {
     const T* f = a.f + (long long)b * a.istride;
     if constexpr (SRC == SRC_PADDED) {
         Padded<T> U{a.upad + (long long)b * a.pstride, a.W}, F{a.fpad + (long long)b * a.pstride, a.W};
-        bpp_body<T, MODE>(U, F, R0, C0, a, sh_rows, sh_vals, &sh_c);
+        bpp_body<T, MODE>(U, F, R0, C0, a, sh_rows, sh_vals, &sh_c, sh_best);
     } else {
         const bool inside = (R0 >= 1) && (C0 >= 1) && (R0 + S < a.m) && (C0 + S < a.n);
         if (inside) {
             Direct<T> U{u, a.n}, F{f, a.n};
-            bpp_body<T, MODE>(U, F, R0, C0, a, sh_rows, sh_vals, &sh_c);
+            bpp_body<T, MODE>(U, F, R0, C0, a, sh_rows, sh_vals, &sh_c, sh_best);
         } else {
             Reflect<T> U{u, a.m, a.n}, F{f, a.m, a.n};
-            bpp_body<T, MODE>(U, F, R0, C0, a, sh_rows, sh_vals, &sh_c);
+            bpp_body<T, MODE>(U, F, R0, C0, a, sh_rows, sh_vals, &sh_c, sh_best);
         }
     }
     __syncthreads();
@@ -608,9 +640,21 @@ __global__ void __launch_bounds__(128) k_sweep_bpp(SweepArgs<T> a) {
     if (threadIdx.x == 0 && !isfinite(c)) a.st[b].bad = 1;
     const int r1 = min(R0 + S, a.m), c1 = min(C0 + S, a.n);
     const int w = c1 - C0, h = r1 - R0;
-    for (int e = threadIdx.x; e < w * h; e += blockDim.x) {
-        T* p = u + (long long)(R0 + e / w) * a.n + (C0 + e % w);
-        *p = X<T>::add(*p, c);
+    // prolongation u += c (hierarchy.py:117-126): a thread per column (w <= 63) and
+    // row lane, eight rows' loads in flight before the first store (the plain
+    // read-modify-write loop made one memory round trip per element)
+    const int col = threadIdx.x & 63, rl = threadIdx.x >> 6, nrl = blockDim.x >> 6;
+    if (col < w) {
+        T* base = u + (long long)R0 * a.n + C0 + col;
+        for (int r = rl; r < h; r += 8 * nrl) {
+            T v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (r + j * nrl < h) v[j] = base[(long long)(r + j * nrl) * a.n];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (r + j * nrl < h) base[(long long)(r + j * nrl) * a.n] = X<T>::add(v[j], c);
+        }
     }
 }
 

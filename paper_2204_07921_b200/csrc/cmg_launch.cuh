@@ -148,16 +148,18 @@ void enqueue_sweep(cmg_plan* P, int layer, int color) {
             dispatch_small_layer<T, MODE_MEAN, PREC_EXACT>(P, a, padded);
     } else {
         const dim3 grd(wc, hc, P->B);
+        // one CTA per patch: 128 threads at level 4 (15 rows, 64 planes), 256 above
+        const int nt = layer >= 5 ? 256 : 128;
         if (P->mode == CMG_MODE_GAUSS) {
             if (padded)
-                klaunch(P, k_sweep_bpp<T, MODE_GAUSS, SRC_PADDED>, grd, 128, 0, a);
+                klaunch(P, k_sweep_bpp<T, MODE_GAUSS, SRC_PADDED>, grd, nt, 0, a);
             else
-                klaunch(P, k_sweep_bpp<T, MODE_GAUSS, SRC_INPLACE>, grd, 128, 0, a);
+                klaunch(P, k_sweep_bpp<T, MODE_GAUSS, SRC_INPLACE>, grd, nt, 0, a);
         } else {
             if (padded)
-                klaunch(P, k_sweep_bpp<T, MODE_MEAN, SRC_PADDED>, grd, 128, 0, a);
+                klaunch(P, k_sweep_bpp<T, MODE_MEAN, SRC_PADDED>, grd, nt, 0, a);
             else
-                klaunch(P, k_sweep_bpp<T, MODE_MEAN, SRC_INPLACE>, grd, 128, 0, a);
+                klaunch(P, k_sweep_bpp<T, MODE_MEAN, SRC_INPLACE>, grd, nt, 0, a);
         }
     }
     P->enq += 1;
