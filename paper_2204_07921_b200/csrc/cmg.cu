@@ -556,11 +556,13 @@ int cmg_plan_create(cmg_plan** out, int m, int n, int batch, int layers, int mod
         P->rp1 |= 2;
     }
     P->rp_nt = n >= 2048 ? 64 : 32;
+    P->rp_nt2 = (n < 2048 && (n + 2) / 3 <= 172) ? 172 : 0;
     if (const char* rp = getenv("CMG_ROWPAIR")) P->rowpair = atoi(rp) & 3;
     if (const char* r1 = getenv("CMG_RP1")) P->rp1 = atoi(r1) & 3;
     if (const char* rb = getenv("CMG_RP_BULK")) P->rp_bulk = atoi(rb);
     if (const char* rt = getenv("CMG_RP_TMA")) P->rp_tma = atoi(rt);
     if (const char* rn = getenv("CMG_RP_NT")) P->rp_nt = atoi(rn);
+    if (const char* rn = getenv("CMG_RP_NT2")) P->rp_nt2 = atoi(rn);
     if (const char* rs = getenv("CMG_RP_STAGES")) P->rp_stages = atoi(rs);
     if (const char* rt = getenv("CMG_RP_TS2")) P->rp_ts2 = atoi(rt);
     if (layers >= 2 && (P->rowpair & 1)) P->fuse_mask |= 2;

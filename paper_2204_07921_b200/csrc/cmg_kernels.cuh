@@ -736,7 +736,7 @@ struct TraceArgs {
 // initial: 1 = record cycle 0, 0 = record the next cycle, 2 = energy-fused
 // cycle (record 0 if the image has not started, else the next cycle; the
 // non-finite flag of the cycle is `bad` | `bad1_prev`).  `shf` is >= NSUM x 256
-// doubles of shared scratch; the first 256 threads reduce (block size >= 256).
+// doubles of shared scratch; the first min(256, block size) threads reduce.
 static __device__ __noinline__ void finalize_image_s(int b, const double* partials, int nbx, const SolveParams* P,
                                               ImgState* st, TraceArgs tr, int initial, double (*shf)[256], int buf) {
     ImgState& S = st[b];
@@ -744,15 +744,19 @@ static __device__ __noinline__ void finalize_image_s(int b, const double* partia
     if (efused) initial = S.started ? 0 : 1;
     if (!initial && tr.eonly == nullptr && tr.raw5 == nullptr && S.done) return;
     const int tid = threadIdx.x;
+    const int nth = min((int)blockDim.x, 256);  // reducing threads (CTAs of fewer than 256 threads: 192)
     double acc[NSUM] = {0, 0, 0, 0, 0};
-    if (tid < 256) {
+    if (tid < nth) {
 #pragma unroll 4
-        for (int i = tid; i < nbx; i += 256)
+        for (int i = tid; i < nbx; i += nth)
 #pragma unroll
             for (int s = 0; s < NSUM; ++s) acc[s] += __ldcg(&partials[((long long)b * nbx + i) * NSUM + s]);
 #pragma unroll
         for (int s = 0; s < NSUM; ++s) shf[s][tid] = acc[s];
     }
+    for (int t = nth + tid; t < 256; t += blockDim.x)  // the tree below runs over 256 slots
+#pragma unroll
+        for (int s = 0; s < NSUM; ++s) shf[s][t] = 0.0;
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
         if (tid < w)

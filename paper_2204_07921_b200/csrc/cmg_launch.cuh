@@ -476,9 +476,9 @@ void launch_rowpair_tma(cmg_plan* P, const T* X, T* Y) {
 }
 
 // persistent bulk-copy variant (one thread per patch, fast mean + f sums)
-template <typename T, int LAYER, int NT, int STAGES>
+template <typename T, int LAYER, int NT, int STAGES, int TPC_ = 0>
 void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y) {
-    using G = RowPairGeom<LAYER, 1, NT, 16 / (int)sizeof(T)>;
+    using G = RowPairGeom<LAYER, 1, NT, 16 / (int)sizeof(T), TPC_>;
     const Level& L = P->lv[LAYER];
     RowPairArgs<T> r;
     r.X = X;
@@ -486,7 +486,7 @@ void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y) {
     r.nj = L.nj;
     r.ntiles = (L.nj + G::TPC - 1) / G::TPC;
     const size_t smem = STAGES * sizeof(T) * G::ROWS * G::WIN;
-    auto kern = k_rowpair_bulk<T, LAYER, NT, STAGES>;
+    auto kern = k_rowpair_bulk<T, LAYER, NT, STAGES, TPC_>;
     smem_attr(kern, smem);
     int occ = 1, nsm = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
@@ -507,12 +507,12 @@ void launch_rowpair_bulk_s(cmg_plan* P, const T* X, T* Y) {
     }
 }
 
-template <typename T, int LAYER, int NT>
+template <typename T, int LAYER, int NT, int TPC_ = 0>
 void launch_rowpair_bulk(cmg_plan* P, const T* X, T* Y) {
     if (P->rp_stages == 1)
-        launch_rowpair_bulk_s<T, LAYER, NT, 1>(P, X, Y);
+        launch_rowpair_bulk_s<T, LAYER, NT, 1, TPC_>(P, X, Y);
     else
-        launch_rowpair_bulk_s<T, LAYER, NT, 2>(P, X, Y);
+        launch_rowpair_bulk_s<T, LAYER, NT, 2, TPC_>(P, X, Y);
 }
 
 template <typename T, int MODE, int PREC>
@@ -523,6 +523,14 @@ void dispatch_rowpair(cmg_plan* P, int layer, const FusedArgs<T>& a) {
         if (((P->rp1 >> (layer - 2)) & 1) && a.fsum) {
             constexpr int NT1 = 64;
             if (P->rp_bulk && ((size_t)P->n * sizeof(T)) % 16 == 0) {
+                // narrow images (64 x 512^2): one 172-patch tile per level-2 patch row with
+                // 128 threads instead of three 62-patch tiles with 32 (87 -> 78 us per visit;
+                // the same at level 3, one 74-patch tile with 64 threads: 116 vs 111 us for
+                // the per-colour team kernels, not kept)
+                if (sizeof(T) == 4 && P->rp_nt2 == 172 && layer == 2 && P->lv[2].nj <= 172) {
+                    launch_rowpair_bulk<T, 2, 128, 172>(P, a.uin, a.uout);
+                    return;
+                }
                 if (sizeof(T) == 4 && P->rp_nt == 128) {
                     if (layer == 2)
                         launch_rowpair_bulk<T, 2, 128>(P, a.uin, a.uout);

@@ -86,6 +86,7 @@ struct cmg_plan {
     int rowpair = 3;        // bit j-2: level j (2, 3) runs as two row-parity launches (k_rowpair)
     bool l1_wide = false;   // k_l1_tile with 32 x 64 tiles (CMG_L1_WIDE)
     int rp_tnt = 128;       // threads per CTA of the bulk-staged level-2 team row-parity kernel (CMG_RP_TNT=256)
+    int rp_nt2 = 0;         // level-2 bulk row-parity kernel: 172 = one 172-patch tile per row (CMG_RP_NT2)
     int l1_th = 0;          // fp64 level-1 tile height override (CMG_L1_TH=28: 28 x 64 tiles)
     bool l1_loop = true;    // fp64 exact mean level 1: branch-free sqrt/div pixel code of cmg_l1loop.cuh
                             // (CMG_L1_LOOP=0: library sqrt/div)

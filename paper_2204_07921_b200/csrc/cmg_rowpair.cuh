@@ -46,12 +46,15 @@ struct WinAcc {
     __device__ __forceinline__ T operator()(int i, int k) const { return s[(i - r0) * ld + (k - k0)]; }
 };
 
-template <int LAYER, int TS, int NT_ = 256, int A_ = 1>
+// TPC_ > 0: fewer owned patch columns than the teams could take (an even count that
+// covers a narrow image in one tile: 64 x 512^2 at level 3 has 74 patch columns)
+template <int LAYER, int TS, int NT_ = 256, int A_ = 1, int TPC_ = 0>
 struct RowPairGeom {
     static constexpr int S = (1 << LAYER) - 1;
     static constexpr int NT = NT_;
     static constexpr int TEAMS = NT / TS;
-    static constexpr int TPC = 2 * TEAMS - 2;          // owned patch columns per CTA (even)
+    static constexpr int TPC = TPC_ > 0 ? TPC_ : 2 * TEAMS - 2;  // owned patch columns per CTA (even)
+    static_assert(TPC % 2 == 0 && TPC <= 2 * TEAMS - 2, "owned patch columns");
     // window columns: [(J0-1)S-1, (J0+TPC+1)S]; with A_ > 1 the window origin is
     // floored to a multiple of A_ elements (16-byte aligned bulk copies) and the
     // width padded to a multiple of A_ that still covers the shifted window
@@ -69,9 +72,9 @@ struct RPItem {
     T* Yb;
 };
 
-template <typename T, int LAYER, int TS, int NT>
+template <typename T, int LAYER, int TS, int NT, int TPC_ = 0>
 __device__ __forceinline__ RPItem<T> rp_item(const RowPairArgs<T>& a, int b, int pr, int tile) {
-    using G = RowPairGeom<LAYER, TS, NT>;
+    using G = RowPairGeom<LAYER, TS, NT, 1, TPC_>;
     constexpr int S = G::S;
     const SweepArgs<T>& A0 = a.c0;
     const int m = A0.m, n = A0.n;
@@ -145,9 +148,10 @@ __device__ __forceinline__ void rp_stage(const RowPairArgs<T>& a, const RPItem<T
 // before; this ends with a barrier-free write-back of owned pixels).
 // EDGES_ONLY: the caller bulk-stores the A-aligned interior of each owned row;
 // the threads write only the (< A) unaligned columns at both ends
-template <typename T, int LAYER, int MODE, int PREC, int TS, int NT, int A = 1, bool EDGES_ONLY = false>
+template <typename T, int LAYER, int MODE, int PREC, int TS, int NT, int A = 1, bool EDGES_ONLY = false,
+          int TPC_ = 0>
 __device__ __forceinline__ void rp_compute(const RowPairArgs<T>& a, const RPItem<T>& it, T* win) {
-    using G = RowPairGeom<LAYER, TS, NT, A>;
+    using G = RowPairGeom<LAYER, TS, NT, A, TPC_>;
     constexpr int S = G::S;
     const SweepArgs<T>& A0 = a.c0;
     const int m = A0.m, n = A0.n, p = A0.p;
@@ -344,11 +348,11 @@ __global__ void __launch_bounds__(NT) k_rowpair_tma(RowPairArgs<T> a) {
 // window row) into two shared-memory stages: item i+1's rows are in flight
 // while item i computes.  u only (no f pixels).  Requires n*sizeof(T) % 16 == 0.
 // ---------------------------------------------------------------------------
-template <typename T, int LAYER, int NT, int STAGES>
+template <typename T, int LAYER, int NT, int STAGES, int TPC_ = 0>
 __global__ void __launch_bounds__(NT) k_rowpair_bulk(RowPairArgs<T> a, int rows, int B) {
     pdl_sync();
     constexpr int A = 16 / (int)sizeof(T);
-    using G = RowPairGeom<LAYER, 1, NT, A>;
+    using G = RowPairGeom<LAYER, 1, NT, A, TPC_>;
     constexpr int STAGE = G::ROWS * G::WIN;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* stage0 = reinterpret_cast<T*>(smem_raw);
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(NT) k_rowpair_bulk(RowPairArgs<T> a, int rows,
         const int b = (int)(itx / per_img);
         const long long r = itx - (long long)b * per_img;
         const int pr = (int)(r / a.ntiles), tile = (int)(r - (long long)pr * a.ntiles);
-        RPItem<T> x = rp_item<T, LAYER, 1, NT>(a, b, pr, tile);
+        RPItem<T> x = rp_item<T, LAYER, 1, NT, TPC_>(a, b, pr, tile);
         x.wk0 = (x.wk0 >= 0) ? (x.wk0 / A) * A : -(((-x.wk0) + A - 1) / A) * A;
         x.border = (x.wr0 < 0) || (x.wr0 + G::ROWS > m) || (x.wk0 < 0) || (x.wk0 + G::WIN > n);
         return x;
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(NT) k_rowpair_bulk(RowPairArgs<T> a, int rows,
         mbar_wait(&full[st], (unsigned)((i / STAGES) & 1));
         T* win = stage0 + st * STAGE;
         if (!a.c0.st[cur.b].done) {
-            rp_compute<T, LAYER, MODE_MEAN, PREC_FAST, 1, NT, A, true>(a, cur, win);
+            rp_compute<T, LAYER, MODE_MEAN, PREC_FAST, 1, NT, A, true, TPC_>(a, cur, win);
             if (tid == 0) store(cur, win);
         }
         __syncthreads();  // the stage is refilled by a later iteration's copy
