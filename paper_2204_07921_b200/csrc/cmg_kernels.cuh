@@ -497,12 +497,21 @@ __global__ void __launch_bounds__(256) k_sweep_team(SweepArgs<T> a) {
     }
     if (!valid || (a.dbg & 4)) return;
     if (lane == 0 && !isfinite(c)) a.st[b].bad = 1;
-    for (int e = lane; e < S * S; e += TS) {
+    // prolongation (hierarchy.py:117-126): the lane's loads are all issued before its
+    // first store (the plain read-modify-write loop made one round trip per element)
+    constexpr int NIT = (S * S + TS - 1) / TS;
+    T v[NIT];
+#pragma unroll
+    for (int t = 0; t < NIT; ++t) {
+        const int e = lane + t * TS;
         const int i = R0 + e / S, k = C0 + e % S;
-        if (i < a.m && k < a.n) {
-            T* p = u + (long long)i * a.n + k;
-            *p = X<T>::add(*p, c);
-        }
+        if (e < S * S && i < a.m && k < a.n) v[t] = u[(long long)i * a.n + k];
+    }
+#pragma unroll
+    for (int t = 0; t < NIT; ++t) {
+        const int e = lane + t * TS;
+        const int i = R0 + e / S, k = C0 + e % S;
+        if (e < S * S && i < a.m && k < a.n) u[(long long)i * a.n + k] = X<T>::add(v[t], c);
     }
 }
 
