@@ -15,6 +15,7 @@
 // through a conditional WHILE node, so one cudaGraphLaunch runs the whole
 // denoise (driver.py:296-310) without host round-trips.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler is attached
 
 #include <cmath>
 #include <cstdio>
@@ -27,6 +28,14 @@
 #include "../../include/cmg.h"
 #include "cmg_plan.h"
 #include "cmg_metrics.cuh"
+
+// NVTX range of one C-ABI call (shows up in Nsight Systems / ncu --nvtx timelines)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 using namespace cmg;
 
@@ -293,6 +302,7 @@ int set_device(cmg_plan* P) {
 int core_solve(cmg_plan* P, bool has_ref, double alpha, double eps, int max_outer, int inner, int stop_rule, int full,
                double peak, double* energy, double* rel_e, double* rel_u, double* psnr, double* seconds,
                int* iterations, int* status) {
+    NvtxRange nvtx("cmg core_solve (V-cycle graph)");
     int rc = check_cfg(alpha, eps, max_outer, inner, stop_rule);
     if (rc) return rc;
     if (!(peak > 0)) return fail(CMG_EINVAL, "peak must be positive");
@@ -758,6 +768,7 @@ int cmg_solve_device(cmg_plan* P, const void* f_dev, const void* ref_dev, void* 
                      double* energy, double* rel_energy, double* rel_u, double* psnr, double* seconds,
                      int* iterations, int* status) {
     if (!P) return fail(CMG_EINVAL, "plan is NULL");
+    NvtxRange nvtx("cmg_solve_device");
     int rc = set_device(P);
     if (rc) return rc;
     const size_t bytes = P->esz * (size_t)P->N * P->B;
@@ -781,6 +792,7 @@ int cmg_solve(cmg_plan* P, const void* f_host, const void* ref_host, void* u_hos
               double* rel_energy, double* rel_u, double* psnr, double* seconds, int* iterations, int* status) {
     if (!P) return fail(CMG_EINVAL, "plan is NULL");
     if (!f_host) return fail(CMG_EINVAL, "f is NULL");
+    NvtxRange nvtx("cmg_solve");
     int rc = set_device(P);
     if (rc) return rc;
     const size_t bytes = P->esz * (size_t)P->N * P->B;
