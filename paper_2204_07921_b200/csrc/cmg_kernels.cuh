@@ -1077,20 +1077,54 @@ __global__ void k_collect(T* u0, const T* u1, const T* u2, long long N, const Im
 }
 
 // Per-patch sums of the odd-padded f of one level (fast mean mode: f* =
-// (sum f - sum u) / S^2, f is constant through a solve).  One thread per patch.
+// (sum f - sum u) / S^2, f is constant through a solve).  One thread per group
+// of four horizontally adjacent patches: inside the image a group's row is
+// 4 S consecutive pixels, read as S 16-byte loads (fp32, rows a multiple of 4
+// pixels long); every pixel is added to its patch's fp64 sum in row-major
+// order, as the one-patch path (groups touching the padding) does.
 template <typename T, int S>
 __global__ void k_patch_fsum(const T* __restrict__ f, double* out, int m, int n, int mj, int nj, long long istride) {
     pdl_sync();
     const int b = blockIdx.y;
     const long long np = (long long)mj * nj;
+    const int ng = (nj + 3) / 4;
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= np) return;
-    const int pr = (int)(e / nj), pc = (int)(e % nj);
-    const Reflect<T> F{f + (long long)b * istride, m, n};
-    double acc = 0.0;
-    for (int i = 0; i < S; ++i)
-        for (int k = 0; k < S; ++k) acc += (double)F(pr * S + i, pc * S + k);
-    out[(long long)b * np + e] = acc;
+    if (e >= (long long)mj * ng) return;
+    const int pr = (int)(e / ng), pc0 = 4 * (int)(e % ng);
+    const T* fb = f + (long long)b * istride;
+    double* ob = out + (long long)b * np + (long long)pr * nj + pc0;
+    if constexpr (sizeof(T) == 4) {
+        if ((n & 3) == 0 && pr * S + S <= m && (pc0 + 4) * S <= n) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            const float4* row = reinterpret_cast<const float4*>(fb + (long long)pr * S * n + (long long)pc0 * S);
+#pragma unroll
+            for (int i = 0; i < S; ++i) {
+                float v[4 * S];
+#pragma unroll
+                for (int q = 0; q < S; ++q) {
+                    const float4 w = __ldg(row + (long long)i * (n / 4) + q);
+                    v[4 * q] = w.x;
+                    v[4 * q + 1] = w.y;
+                    v[4 * q + 2] = w.z;
+                    v[4 * q + 3] = w.w;
+                }
+#pragma unroll
+                for (int pp = 0; pp < 4; ++pp)
+#pragma unroll
+                    for (int k = 0; k < S; ++k) acc[pp] += (double)v[pp * S + k];
+            }
+#pragma unroll
+            for (int pp = 0; pp < 4; ++pp) ob[pp] = acc[pp];
+            return;
+        }
+    }
+    const Reflect<T> F{fb, m, n};
+    for (int pp = 0; pp < 4 && pc0 + pp < nj; ++pp) {
+        double acc = 0.0;
+        for (int i = 0; i < S; ++i)
+            for (int k = 0; k < S; ++k) acc += (double)F(pr * S + i, (pc0 + pp) * S + k);
+        ob[pp] = acc;
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -120,7 +120,7 @@ void enqueue_fsums(cmg_plan* P) {
     for (int j = 2; j <= std::min(P->layers, 3); ++j) {
         if (!P->fsum[j]) continue;
         const Level& L = P->lv[j];
-        const long long np = (long long)L.mj * L.nj;
+        const long long np = (long long)L.mj * ((L.nj + 3) / 4);  // one thread per group of four patches
         const dim3 grd((unsigned)((np + 255) / 256), P->B);
         if (j == 2)
             klaunch(P, k_patch_fsum<T, 3>, grd, 256, 0, (const T*)P->f, P->fsum[j], P->m, P->n, L.mj, L.nj, P->N);
