@@ -953,6 +953,9 @@ __device__ __forceinline__ void cta_sums_store(const double (&acc)[NSUM], double
             for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
             if (lane == 0) partials[((long long)b * nbx + cta) * NSUM + s] = v;
         }
+        // the writer fences here, long before its ticket (efused_ticket): the image's last
+        // CTA then sees every CTA's sums without an all-thread fence behind the tile stores
+        if (lane == 0) __threadfence();
     }
 }
 
@@ -964,7 +967,9 @@ __device__ __forceinline__ void efused_ticket(const EnergyFin& fz, const double*
                                               double* scratch) {
     __shared__ int last;
     const int tid = threadIdx.x;
-    __threadfence();
+    // (thread 0 wrote and fenced this CTA's sums in cta_sums_store and fences its
+    // non-finite flag where it sets it; the tile stores need no fence: nothing
+    // before the next kernel reads them)
     __syncthreads();
     if (tid == 0) last = (atomicAdd(&fz.tickets[b], 1) == nbx - 1);
     __syncthreads();

@@ -376,10 +376,12 @@ __global__ void __launch_bounds__(256, MODE == MODE_MEAN ? 4 : 1) k_l1_tile(Fuse
         if (border) l1_reflect_fix<T, TH, TW>(su, r0, c0, m, n);
     });
     if (__syncthreads_or(bad) && threadIdx.x == 0) {
-        if (a.efuse)
+        if (a.efuse) {
             a.st[b].bad1 = 1;
-        else
+            __threadfence();  // visible to the CTA that finalizes (efused_ticket)
+        } else {
             a.st[b].bad = 1;
+        }
     }
     for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
         const int i = e / TW, k = e % TW;

@@ -444,10 +444,12 @@ __global__ void __launch_bounds__(NT) k_l1_x2(FusedArgs<float> a) {
     f2_unpack(finite_acc, fa0, fa1);
     const bool bad = !(isfinite(fa0) && isfinite(fa1));
     if (__syncthreads_or(bad) && threadIdx.x == 0) {
-        if constexpr (EF)
+        if constexpr (EF) {
             a.st[b].bad1 = 1;
-        else
+            __threadfence();  // visible to the CTA that finalizes (efused_ticket)
+        } else {
             a.st[b].bad = 1;
+        }
     }
     if constexpr (EF) {
         __syncthreads();  // shared memory becomes the finalize scratch
