@@ -423,6 +423,20 @@ def run_ours(args):
             pd = json.loads(pipes.read_text()).get(key)
             if pd:
                 line["roofline"]["compute"] = pd
+        if args.dtype == "float64" and "compute" in line["roofline"]:
+            # the compute roof, measured live: sustained DFMA rate and dependent-chain
+            # latency of the FP64 pipe (cmg_fp64_probe)
+            pr = N.fp64_probe(local)
+            cp = line["roofline"]["compute"]
+            cp["fp64_probe"] = pr
+            if cp.get("fp64_thread_instr_per_launch") and cp.get("ncu_cold_us"):
+                import torch
+
+                props = torch.cuda.get_device_properties(local)
+                rate = cp["fp64_thread_instr_per_launch"] / (cp["ncu_cold_us"] * 1e-6) / (
+                    clocks.get("sm_mhz", 1965.0) * 1e6) / props.multi_processor_count
+                cp["fp64_instr_per_clk_per_sm"] = rate  # energy-fused kernel, ncu (cold) duration
+                cp["fp64_frac_of_probe"] = rate / pr["dfma_per_clk_per_sm"]
     if args.config == 3 and args.dtype == "float64" and args.precision == "exact":
         line["roofline"]["note"] = ("1024^2 fp64 exact: u and f (16 MiB) stay in the 126 MB L2; the level-1 "
                                     "kernel is FP64-pipe / latency bound (8 correctly rounded sqrt + 10 div per "

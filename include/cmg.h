@@ -206,6 +206,16 @@ int cmg_host_free(void* p);
 int cmg_l2_read_bandwidth(int device, long long bytes, int reps, double* gbs);
 
 /*
+ * Measurement helper (no reference counterpart): the FP64 pipe of the device,
+ * the compute roof of the fp64 exact level-1 kernel.  *dfma_per_clk_per_sm =
+ * sustained thread-level DFMAs per clock and SM (64 warps per SM, 8
+ * independent chains per thread, CUDA events, nominal SM clock), *tflops the
+ * same as 2 x DFMA/s, *dep_latency_cycles = clocks per DFMA of one dependent
+ * chain in one warp (clock64).
+ */
+int cmg_fp64_probe(int device, double* dfma_per_clk_per_sm, double* dep_latency_cycles, double* tflops);
+
+/*
  * Self test (no reference counterpart) of the branch-free correctly rounded
  * fp64 sqrt / div that the level-1 exact kernel uses (csrc/cmg_l1loop.cuh)
  * against the device library's sqrt.rn / div.rn on n host operand pairs:

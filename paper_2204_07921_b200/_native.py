@@ -25,7 +25,7 @@ SYMBOLS = (
     "cmg_solve_device", "cmg_sweep_layer", "cmg_energy", "cmg_plane_table", "cmg_plan_stats", "cmg_time_sweep",
     "cmg_host_alloc", "cmg_host_free", "cmg_plan_buffer", "cmg_buffer_upload", "cmg_buffer_download",
     "cmg_level_step", "cmg_energy_partials", "cmg_ssim_batch", "cmg_plan_ssim", "cmg_l2_read_bandwidth",
-    "cmg_selftest_exact",
+    "cmg_selftest_exact", "cmg_fp64_probe",
     "cmg_plan_stream", "cmg_strip_begin", "cmg_level_step_async", "cmg_strip_partials_async", "cmg_strip_read",
     "cmg_mplan_create", "cmg_mplan_destroy", "cmg_mplan_solve",
     "cmg_radon_create", "cmg_radon_destroy", "cmg_radon_forward", "cmg_radon_adjoint", "cmg_recon_chalf",
@@ -107,6 +107,8 @@ def _declare(L):
     L.cmg_strip_read.argtypes = [_vp, _dp]
     L.cmg_l2_read_bandwidth.restype = _i
     L.cmg_l2_read_bandwidth.argtypes = [_i, ctypes.c_longlong, _i, _dp]
+    L.cmg_fp64_probe.restype = _i
+    L.cmg_fp64_probe.argtypes = [_i, _dp, _dp, _dp]
     L.cmg_selftest_exact.restype = _i
     L.cmg_selftest_exact.argtypes = [_i, _dp, _dp, ctypes.c_longlong, ctypes.POINTER(ctypes.c_ulonglong)]
     L.cmg_host_free.restype = _i
@@ -220,6 +222,16 @@ def l2_read_bandwidth(device: int = 0, nbytes: int = 32 << 20, reps: int = 50) -
     if rc != CMG_OK:
         raise RuntimeError(last_error())
     return out.value
+
+
+def fp64_probe(device: int = 0) -> dict:
+    """cmg_fp64_probe: sustained DFMA rate (per clock and SM, and as TFLOP/s) and the
+    dependent-chain latency of the device's FP64 pipe."""
+    r, lat, tf = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_double(0)
+    rc = lib().cmg_fp64_probe(device, ctypes.byref(r), ctypes.byref(lat), ctypes.byref(tf))
+    if rc != CMG_OK:
+        raise RuntimeError(last_error())
+    return {"dfma_per_clk_per_sm": r.value, "dep_latency_cycles": lat.value, "tflops": tf.value}
 
 
 def selftest_exact(a, b, device: int = 0):

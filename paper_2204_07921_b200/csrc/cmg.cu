@@ -111,6 +111,25 @@ __global__ void k_l2_read(const uint4* __restrict__ buf, long long n16, int reps
     if (acc == 0x9e3779b9u) sink[(blockIdx.x * blockDim.x + threadIdx.x) & 1048575] = acc;
 }
 
+// FP64 pipe probe: ILP independent chains of dependent DFMAs per thread
+template <int ILP>
+__global__ void k_fp64_chain(double* out, int iters, double a, double b, long long* cycles) {
+    double x[ILP];
+#pragma unroll
+    for (int j = 0; j < ILP; ++j) x[j] = (double)(threadIdx.x + j) * 1e-3;
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < ILP; ++j) x[j] = __fma_rn(x[j], a, b);
+    }
+    const long long t1 = clock64();
+    double sum = 0.0;
+#pragma unroll
+    for (int j = 0; j < ILP; ++j) sum += x[j];
+    if (sum == 12345.678) out[blockIdx.x * blockDim.x + threadIdx.x] = sum;
+    if (cycles && blockIdx.x == 0 && threadIdx.x == 0) *cycles = t1 - t0;
+}
+
 std::vector<int> layer_sequence(int layers, int full) {
     std::vector<int> s;
     for (int j = 1; j <= layers; ++j) s.push_back(j);
@@ -1174,6 +1193,49 @@ int cmg_l2_read_bandwidth(int device, long long bytes, int reps, double* gbs) {
     cudaFree(sink);
     if (e != cudaSuccess) return fail(CMG_ECUDA, cudaGetErrorString(e));
     *gbs = (double)n16 * 16.0 * reps / (ms * 1e-3) / 1e9;
+    return CMG_OK;
+}
+
+int cmg_fp64_probe(int device, double* dfma_per_clk_per_sm, double* dep_latency_cycles, double* tflops) {
+    if (!dfma_per_clk_per_sm || !dep_latency_cycles || !tflops) return fail(CMG_EINVAL, "NULL argument");
+    CK(cudaSetDevice(device));
+    int nsm = 0, khz = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device));
+    double* out = nullptr;
+    long long* cyc = nullptr;
+    CK(cudaMalloc(&out, sizeof(double) * (size_t)nsm * 4 * 1024));
+    if (cudaMalloc(&cyc, sizeof(long long)) != cudaSuccess) {
+        cudaFree(out);
+        return fail(CMG_ECUDA, "cudaMalloc");
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 4096;
+    // latency: one warp, one chain; (cycles between the clock reads) / iters
+    k_fp64_chain<1><<<1, 32>>>(out, iters, 0.999, 1e-9, cyc);
+    k_fp64_chain<1><<<1, 32>>>(out, iters, 0.999, 1e-9, cyc);
+    long long hc = 0;
+    cudaError_t e = cudaMemcpy(&hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
+    // throughput: 4 CTAs of 1024 threads per SM (all 64 warps), 8 chains per thread
+    k_fp64_chain<8><<<nsm * 4, 1024>>>(out, 64, 0.999, 1e-9, nullptr);
+    cudaEventRecord(e0);
+    k_fp64_chain<8><<<nsm * 4, 1024>>>(out, iters, 0.999, 1e-9, nullptr);
+    cudaEventRecord(e1);
+    if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    cudaFree(cyc);
+    if (e != cudaSuccess) return fail(CMG_ECUDA, cudaGetErrorString(e));
+    const double dfma = (double)nsm * 4 * 1024 * 8.0 * iters;  // thread-level DFMAs
+    *dep_latency_cycles = (double)hc / iters;
+    *tflops = 2.0 * dfma / (ms * 1e-3) / 1e12;
+    *dfma_per_clk_per_sm = dfma / (ms * 1e-3) / ((double)khz * 1e3) / nsm;
     return CMG_OK;
 }
 
